@@ -1,0 +1,320 @@
+"""Python front end over the C-ABI (device tensors in, device tensors out).
+
+Mirrors the reference's operator surface for the hot path
+(/root/reference/proj/include/mp): ``isgmr_forward`` / ``trwp_forward``
+(isgmr.hpp:145-152, trwp.hpp:148-156), ``isgmr_backward`` / ``trwp_backward``
+(autodiff.hpp:63-197), the engine ``step()`` / ``aggregate()`` pair
+(isgmr.hpp:49-59, trwp.hpp:47-61) and ``GridTopology`` (grid.hpp:73-96), with
+a leading batch dimension. Argument meaning follows the reference; invalid
+arguments raise ``MrfInvalidArgument`` (a ``ValueError``) where the reference
+throws ``std::invalid_argument``.
+
+PyTorch is only the device-memory / stream plumbing here: every computation
+runs in libmrf_cuda.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ENGINE_ISGMR, ENGINE_TRWP, check, lib
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class GridTopology:
+    """Scanline geometry for an H x W grid with 4/8/16 connectivity
+    (mp::GridTopology, grid.hpp:73-96; identical scanline order and edge ids)."""
+
+    def __init__(self, height: int, width: int, connectivity: int):
+        h = C.c_void_p()
+        check(lib().mrf_topology_create(height, width, connectivity, C.byref(h)))
+        self._h = h
+        self.height, self.width, self.connectivity = height, width, connectivity
+        nd = C.c_int()
+        te = C.c_int64()
+        self.edge_count = np.zeros(connectivity, np.int64)
+        self.dir_offset = np.zeros(connectivity, np.int64)
+        check(lib().mrf_topology_info(h, C.byref(nd), C.byref(te),
+                                      self.edge_count.ctypes.data_as(C.POINTER(C.c_int64)),
+                                      self.dir_offset.ctypes.data_as(C.POINTER(C.c_int64))))
+        self.num_dirs = nd.value
+        self.total_edges = te.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def nodes(self):
+        return self.height * self.width
+
+    def edge_index(self) -> np.ndarray:
+        out = np.zeros((self.num_dirs, self.nodes), np.int32)
+        check(lib().mrf_topology_edge_index(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def scanlines(self, r: int):
+        cnt = C.c_int32()
+        check(lib().mrf_topology_scanlines(self._h, r, None, None, C.byref(cnt), 0))
+        first = np.zeros(cnt.value, np.int32)
+        length = np.zeros(cnt.value, np.int32)
+        check(lib().mrf_topology_scanlines(self._h, r, first.ctypes.data_as(C.c_void_p),
+                                           length.ctypes.data_as(C.c_void_p), C.byref(cnt), cnt.value))
+        return first, length
+
+    def index_bytes(self, labels: int, iterations: int) -> int:
+        """IndexStore::bytes() == K * sum_r |E^r| * (L + 1) (index_store.hpp:11-15)."""
+        return iterations * self.total_edges * (labels + 1)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().mrf_topology_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+@dataclass
+class MRF:
+    """A batch of MRF instances sharing one topology and one pairwise table.
+
+    unary   [B, N, L] float32 cuda       (UnaryVolume::values)
+    V       [L, L]    float32 cuda       (PairwiseFunction::table)
+    weight  float, or [B, R/2, N] tensor (EdgeWeights constant / planes)
+    rho     float, or [B, R/2, N] tensor (TreeCoefficients, TRWP only)
+    """
+
+    topo: GridTopology
+    unary: torch.Tensor
+    V: torch.Tensor
+    weight: float | torch.Tensor = 1.0
+    rho: float | torch.Tensor = 0.5
+
+    def __post_init__(self):
+        t = self.topo
+        if self.unary.dim() == 2:
+            self.unary = self.unary.unsqueeze(0)
+        if self.unary.dim() != 3 or self.unary.shape[1] != t.nodes:
+            raise ValueError("unary must be [B, H*W, L]")
+        for name in ("unary", "V"):
+            x = getattr(self, name)
+            if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+        L = self.labels
+        if tuple(self.V.shape) != (L, L):
+            raise ValueError("V must be [L, L]")
+        for name in ("weight", "rho"):
+            x = getattr(self, name)
+            if isinstance(x, torch.Tensor):
+                if x.dim() == 2:
+                    x = x.unsqueeze(0)
+                    setattr(self, name, x)
+                if tuple(x.shape) != (self.batch, t.num_dirs // 2, t.nodes) or x.dtype != torch.float32 \
+                        or not x.is_cuda or not x.is_contiguous():
+                    raise ValueError(f"{name} planes must be contiguous float32 CUDA [B, R/2, N]")
+
+    @property
+    def batch(self):
+        return self.unary.shape[0]
+
+    @property
+    def labels(self):
+        return self.unary.shape[2]
+
+    def c_problem(self) -> _lib.Problem:
+        t = self.topo
+        wt = self.weight if isinstance(self.weight, torch.Tensor) else None
+        rt = self.rho if isinstance(self.rho, torch.Tensor) else None
+        return _lib.Problem(self.batch, t.height, t.width, self.labels, self.unary.data_ptr(), self.V.data_ptr(),
+                            0.0 if wt is not None else float(self.weight), None if wt is None else wt.data_ptr(),
+                            0.5 if rt is not None else float(self.rho), None if rt is None else rt.data_ptr())
+
+
+@dataclass
+class ForwardResult:
+    """mp::ForwardResult (inference.hpp:62-68) for a batch: cost [B,N,L],
+    labels [B,N] (int32 view of uint16), messages [B,R,N,L], p [B,K,E,L],
+    q [B,K,E]."""
+
+    cost: torch.Tensor
+    labels: torch.Tensor
+    messages: torch.Tensor
+    p: torch.Tensor
+    q: torch.Tensor
+    iterations: int
+
+
+@dataclass
+class GradientSet:
+    """mp::GradientSet (autodiff.hpp:17-29): unary [B,N,L], pairwise [B,L,L],
+    edge_weights [B,R/2,N]."""
+
+    unary: torch.Tensor
+    pairwise: torch.Tensor
+    edge_weights: torch.Tensor
+
+    def edge_weight_total(self):
+        return self.edge_weights.sum(dim=(1, 2))
+
+
+def _alloc_forward(mrf: MRF, K: int):
+    t, B, L = mrf.topo, mrf.batch, mrf.labels
+    dev = mrf.unary.device
+    return ForwardResult(
+        cost=torch.empty((B, t.nodes, L), dtype=torch.float32, device=dev),
+        labels=torch.empty((B, t.nodes), dtype=torch.int16, device=dev),
+        messages=torch.empty((B, t.num_dirs, t.nodes, L), dtype=torch.float32, device=dev),
+        p=torch.empty((B, K, t.total_edges, L), dtype=torch.uint8, device=dev),
+        q=torch.empty((B, K, t.total_edges), dtype=torch.uint8, device=dev),
+        iterations=K)
+
+
+def _forward(engine: int, mrf: MRF, K: int, out: ForwardResult | None, stream):
+    if K < 1:
+        raise _lib.MrfInvalidArgument(1, "iterations must be >= 1")
+    out = out or _alloc_forward(mrf, K)
+    pr = mrf.c_problem()
+    wsb = lib().mrf_forward_workspace_bytes(mrf.topo.handle, C.byref(pr), engine, K)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=mrf.unary.device)
+    fo = _lib.ForwardOut(_ptr(out.cost), _ptr(out.labels), _ptr(out.messages), _ptr(out.p), _ptr(out.q))
+    fn = lib().mrf_isgmr_forward_f32 if engine == ENGINE_ISGMR else lib().mrf_trwp_forward_f32
+    check(fn(mrf.topo.handle, C.byref(pr), K, C.byref(fo), _ptr(ws), wsb, _stream(stream)))
+    out._workspace = ws  # keep alive until the stream consumes it
+    return out
+
+
+def isgmr_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None) -> ForwardResult:
+    """mp::isgmr_forward<float> (isgmr.hpp:145-152) for a batch."""
+    return _forward(ENGINE_ISGMR, mrf, iterations, out, stream)
+
+
+def trwp_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None) -> ForwardResult:
+    """mp::trwp_forward<float> (trwp.hpp:148-156) for a batch; rho from mrf.rho."""
+    return _forward(ENGINE_TRWP, mrf, iterations, out, stream)
+
+
+def _backward(engine: int, mrf: MRF, fwd_p, fwd_q, K: int, grad_cost, out: GradientSet | None, stream):
+    t, B, L = mrf.topo, mrf.batch, mrf.labels
+    dev = mrf.unary.device
+    if grad_cost.shape != mrf.unary.shape:
+        raise _lib.MrfInvalidArgument(1, "backward: cost gradient size mismatch")
+    grad_cost = grad_cost.contiguous()
+    out = out or GradientSet(torch.empty_like(mrf.unary), torch.empty((B, L, L), dtype=torch.float32, device=dev),
+                             torch.empty((B, t.num_dirs // 2, t.nodes), dtype=torch.float32, device=dev))
+    pr = mrf.c_problem()
+    wsb = lib().mrf_backward_workspace_bytes(t.handle, C.byref(pr), engine, K)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    g = _lib.Grads(_ptr(out.unary), _ptr(out.pairwise), _ptr(out.edge_weights))
+    fn = lib().mrf_isgmr_backward_f32 if engine == ENGINE_ISGMR else lib().mrf_trwp_backward_f32
+    check(fn(t.handle, C.byref(pr), K, _ptr(fwd_p), _ptr(fwd_q), _ptr(grad_cost), C.byref(g), _ptr(ws), wsb,
+             _stream(stream)))
+    out._workspace = ws
+    return out
+
+
+def isgmr_backward(mrf: MRF, fwd: ForwardResult, grad_cost, out=None, stream=None) -> GradientSet:
+    """mp::isgmr_backward<float> (autodiff.hpp:63-126) for a batch."""
+    return _backward(ENGINE_ISGMR, mrf, fwd.p, fwd.q, fwd.iterations, grad_cost, out, stream)
+
+
+def trwp_backward(mrf: MRF, fwd: ForwardResult, grad_cost, out=None, stream=None) -> GradientSet:
+    """mp::trwp_backward<float> (autodiff.hpp:133-197) for a batch."""
+    return _backward(ENGINE_TRWP, mrf, fwd.p, fwd.q, fwd.iterations, grad_cost, out, stream)
+
+
+def aggregate(mrf: MRF, messages, cost=None, labels=None, stream=None):
+    """aggregate_costs + argmin_labels (inference.hpp:25-57)."""
+    t = mrf.topo
+    cost = cost if cost is not None else torch.empty_like(mrf.unary)
+    labels = labels if labels is not None else torch.empty((mrf.batch, t.nodes), dtype=torch.int16,
+                                                           device=mrf.unary.device)
+    pr = mrf.c_problem()
+    check(lib().mrf_aggregate_f32(t.handle, C.byref(pr), _ptr(messages), _ptr(cost), _ptr(labels), _stream(stream)))
+    return cost, labels
+
+
+class IsgmrEngine:
+    """mp::IsgmrEngine (isgmr.hpp:26-143): step() runs one iteration,
+    aggregate() returns (cost, labels). Index capacity is fixed up front."""
+
+    def __init__(self, mrf: MRF, max_iterations: int):
+        t = mrf.topo
+        self.mrf, self.K_cap, self.k = mrf, max_iterations, 0
+        shape = (mrf.batch, t.num_dirs, t.nodes, mrf.labels)
+        self.m = torch.zeros(shape, dtype=torch.float32, device=mrf.unary.device)
+        self.mhat = torch.zeros(shape, dtype=torch.float32, device=mrf.unary.device)
+        self.p = torch.empty((mrf.batch, max_iterations, t.total_edges, mrf.labels), dtype=torch.uint8,
+                             device=mrf.unary.device)
+        self.q = torch.empty((mrf.batch, max_iterations, t.total_edges), dtype=torch.uint8, device=mrf.unary.device)
+
+    def step(self, stream=None):
+        if self.k >= self.K_cap:
+            raise _lib.MrfInvalidArgument(1, "index store capacity exhausted")
+        pr = self.mrf.c_problem()
+        check(lib().mrf_isgmr_step_f32(self.mrf.topo.handle, C.byref(pr), self.k, self.K_cap, _ptr(self.m),
+                                       _ptr(self.mhat), _ptr(self.p), _ptr(self.q), _stream(stream)))
+        self.m, self.mhat = self.mhat, self.m  # publish m <- mhat (isgmr.hpp:55)
+        self.k += 1
+
+    def messages(self):
+        return self.m
+
+    def aggregate(self, stream=None):
+        return aggregate(self.mrf, self.m, stream=stream)
+
+
+class TrwpEngine:
+    """mp::TrwpEngine (trwp.hpp:25-146)."""
+
+    def __init__(self, mrf: MRF, max_iterations: int):
+        t = mrf.topo
+        self.mrf, self.K_cap, self.k = mrf, max_iterations, 0
+        self.m = torch.zeros((mrf.batch, t.num_dirs, t.nodes, mrf.labels), dtype=torch.float32,
+                             device=mrf.unary.device)
+        self.p = torch.empty((mrf.batch, max_iterations, t.total_edges, mrf.labels), dtype=torch.uint8,
+                             device=mrf.unary.device)
+        self.q = torch.empty((mrf.batch, max_iterations, t.total_edges), dtype=torch.uint8, device=mrf.unary.device)
+
+    def step(self, stream=None):
+        if self.k >= self.K_cap:
+            raise _lib.MrfInvalidArgument(1, "index store capacity exhausted")
+        pr = self.mrf.c_problem()
+        check(lib().mrf_trwp_step_f32(self.mrf.topo.handle, C.byref(pr), self.k, self.K_cap, _ptr(self.m),
+                                      _ptr(self.p), _ptr(self.q), _stream(stream)))
+        self.k += 1
+
+    def messages(self):
+        return self.m
+
+    def aggregate(self, stream=None):
+        return aggregate(self.mrf, self.m, stream=stream)
+
+
+def check_finite(x: torch.Tensor, stream=None) -> bool:
+    flag = C.c_int()
+    check(lib().mrf_check_finite_f32(_ptr(x), x.numel(), C.byref(flag), _stream(stream)))
+    return bool(flag.value)
+
+
+def pack_shared_grads(mrf: MRF, grads: GradientSet, out=None, stream=None):
+    """[sum_b dV_b (L*L), sum of dw planes] -- the buffer one all-reduce sums."""
+    L = mrf.labels
+    out = out if out is not None else torch.empty(L * L + 1, dtype=torch.float32, device=mrf.unary.device)
+    pr = mrf.c_problem()
+    g = _lib.Grads(_ptr(grads.unary), _ptr(grads.pairwise), _ptr(grads.edge_weights))
+    check(lib().mrf_pack_shared_grads_f32(C.byref(pr), mrf.topo.num_dirs, C.byref(g), _ptr(out), _stream(stream)))
+    return out

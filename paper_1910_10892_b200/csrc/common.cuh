@@ -1,0 +1,58 @@
+// Shared device helpers for the message-passing kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mrf {
+
+constexpr int kMaxDirs = 16;
+
+// Everything a sweep kernel needs to address one image's tensors. Strides are
+// per image (batch index = blockIdx.y).
+struct Geometry {
+  int N, L, R, W;
+  int K_cap;                       // iterations the index store holds
+  int64_t E;                       // total edges per iteration
+  int64_t dir_offset[kMaxDirs];    // IndexStore::dir_offset(r)
+  int node_step[kMaxDirs];         // dh*W + dw
+};
+
+struct Potentials {
+  const float* unary;      // [B][N][L]
+  const float* V;          // [L][L]
+  float w;                 // constant weight (w_planes == nullptr)
+  const float* w_planes;   // [B][R/2][N]
+  float rho;               // constant rho (rho_planes == nullptr)
+  const float* rho_planes; // [B][R/2][N]
+};
+
+// A scanline with at least one edge: head node, node count, edge base, direction.
+struct __align__(16) LineDesc {
+  int32_t first, length, edge_base, dir;
+};
+
+__device__ __forceinline__ float plane_value(const float* planes, float c, int N, int R, int b, int r, int prev,
+                                             int cur) {
+  if (planes == nullptr) return c;
+  return __ldg(planes + (size_t(b) * (R / 2) + (r >> 1)) * N + ((r & 1) ? cur : prev));
+}
+
+// Monotone float -> uint32 map (non-NaN inputs). -0 is folded onto +0 by the
+// caller (v + 0.0f) so that equal values compare equal, as the reference's
+// strict '<' scans treat them.
+__device__ __forceinline__ uint32_t order_key(float v) {
+  const uint32_t u = __float_as_uint(v);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_value(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// No FMA contraction anywhere on the path: one rounding per operation, in the
+// reference's order (SURVEY.md §7 hard part 1).
+__device__ __forceinline__ float fadd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }
+
+}  // namespace mrf

@@ -1,0 +1,91 @@
+// Small C-ABI utilities: finiteness scan, shared-gradient packing and the one
+// data-parallel collective (NCCL all-reduce, resolved at run time).
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <string>
+
+#include "../../include/mrf_cuda.h"
+#include "common.cuh"
+
+namespace {
+
+__global__ void finite_kernel(const float* __restrict__ x, size_t n, int* flag) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const uint32_t u = __float_as_uint(x[i]);
+    if ((u & 0x7f800000u) == 0x7f800000u) {
+      *flag = 0;
+      return;
+    }
+  }
+}
+
+// out[0:L*L] = sum_b pairwise[b] (b ascending); out[L*L] = sum of all weight
+// planes (GradientSet::edge_weight_total, autodiff.hpp:24-28), one block.
+__global__ void pack_kernel(int B, int L, int64_t plane_elems, const float* __restrict__ gv, const float* __restrict__ gw,
+                            float* __restrict__ out) {
+  const int LL = L * L;
+  for (int i = threadIdx.x; i < LL; i += blockDim.x) {
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s = mrf::fadd(s, gv[size_t(b) * LL + i]);
+    out[i] = s;
+  }
+  __shared__ float part[1024];
+  float s = 0.0f;
+  if (gw)
+    for (int64_t i = threadIdx.x; i < int64_t(B) * plane_elems; i += blockDim.x) s = mrf::fadd(s, gw[i]);
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int i = 0; i < int(blockDim.x); ++i) t = mrf::fadd(t, part[i]);
+    out[LL] = t;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaStream_t stream) {
+  if (!data || !all_finite) return MRF_EINVAL;
+  int* dflag = nullptr;
+  cudaError_t e = cudaMallocAsync(&dflag, sizeof(int), stream);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? MRF_ENOMEM : MRF_ECUDA;
+  const int one = 1;
+  cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, stream);
+  if (count) finite_kernel<<<1184, 256, 0, stream>>>(data, count, dflag);
+  int h = 0;
+  cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream);
+  cudaFreeAsync(dflag, stream);
+  e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return MRF_ECUDA;
+  *all_finite = h;
+  return MRF_OK;
+}
+
+int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const mrf_grads_f32* grads, float* out,
+                              cudaStream_t stream) {
+  if (!prob || !grads || !grads->pairwise || !out || prob->batch < 1 || prob->labels < 1) return MRF_EINVAL;
+  const int64_t plane_elems = int64_t(num_dirs / 2) * prob->height * prob->width;
+  pack_kernel<<<1, 1024, 0, stream>>>(prob->batch, prob->labels, plane_elems, grads->pairwise, grads->weight_planes,
+                                      out);
+  return cudaGetLastError() == cudaSuccess ? MRF_OK : MRF_ECUDA;
+}
+
+int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream) {
+  // ncclAllReduce(sendbuff, recvbuff, count, ncclFloat=7, ncclSum=0, comm, stream)
+  using AllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+  static AllReduceFn fn = nullptr;
+  if (!nccl_comm || !buffer) return MRF_EINVAL;
+  if (!fn) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return MRF_ECUDA;
+    fn = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
+    if (!fn) return MRF_ECUDA;
+  }
+  return fn(buffer, buffer, count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, nccl_comm, stream) == 0 ? MRF_OK : MRF_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,439 @@
+// libmrf_cuda.so: C-ABI entry points (include/mrf_cuda.h) over the sm_100a
+// message-passing kernels. Host code here only validates, plans launches and
+// owns the per-device topology upload; all arithmetic runs on the GPU.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mrf_cuda.h"
+#include "common.cuh"
+#include "kernels_v1.cuh"
+#include "topology.hpp"
+
+using namespace mrf;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct MrfError : std::runtime_error {
+  int code;
+  MrfError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw MrfError(code, msg); }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    fail(e == cudaErrorMemoryAllocation ? MRF_ENOMEM : MRF_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MRF_OK;
+  } catch (const MrfError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return MRF_EINVAL;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return MRF_ENOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return MRF_ECUDA;
+  }
+}
+
+constexpr int kBwdSlots = 592;  // 4 x 148 SMs: persistent backward CTAs per image
+
+}  // namespace
+
+// Topology handle: host geometry plus lazily uploaded per-device line tables.
+struct mrf_topology_s {
+  Topology host;
+  std::vector<LineDesc> all_lines;                 // ISGMR: every direction, longest first
+  std::vector<std::vector<LineDesc>> dir_lines;    // per direction, longest first
+  std::vector<size_t> dir_start;                   // offset of dir r's block in the upload
+  struct Dev {
+    LineDesc* lines = nullptr;  // [all_lines | dir 0 | dir 1 | ...]
+  };
+  std::map<int, Dev> dev;
+  std::mutex mu;
+
+  mrf_topology_s(int H, int W, int conn) : host(H, W, conn) {
+    dir_lines.resize(host.num_dirs());
+    for (int r = 0; r < host.num_dirs(); ++r) {
+      for (const Line& l : host.lines(r))
+        if (l.length >= 2) dir_lines[r].push_back({l.first, l.length, l.edge_base, r});
+      std::stable_sort(dir_lines[r].begin(), dir_lines[r].end(),
+                       [](const LineDesc& a, const LineDesc& b) { return a.length > b.length; });
+      all_lines.insert(all_lines.end(), dir_lines[r].begin(), dir_lines[r].end());
+    }
+    std::stable_sort(all_lines.begin(), all_lines.end(),
+                     [](const LineDesc& a, const LineDesc& b) { return a.length > b.length; });
+    size_t off = all_lines.size();
+    for (int r = 0; r < host.num_dirs(); ++r) {
+      dir_start.push_back(off);
+      off += dir_lines[r].size();
+    }
+  }
+
+  ~mrf_topology_s() {
+    for (auto& kv : dev) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(kv.first);
+      cudaFree(kv.second.lines);
+      cudaSetDevice(cur);
+    }
+  }
+
+  const LineDesc* device_lines() {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(d);
+    if (it != dev.end()) return it->second.lines;
+    std::vector<LineDesc> all(all_lines);
+    for (auto& v : dir_lines) all.insert(all.end(), v.begin(), v.end());
+    Dev dv;
+    cuda_check(cudaMalloc(&dv.lines, sizeof(LineDesc) * std::max<size_t>(1, all.size())), "cudaMalloc(lines)");
+    cuda_check(cudaMemcpy(dv.lines, all.data(), sizeof(LineDesc) * all.size(), cudaMemcpyHostToDevice),
+               "upload lines");
+    dev[d] = dv;
+    return dv.lines;
+  }
+};
+
+namespace {
+
+void validate_problem(mrf_topology_t topo, const mrf_problem_f32* pr) {
+  if (!topo) fail(MRF_EINVAL, "null topology");
+  if (!pr) fail(MRF_EINVAL, "null problem");
+  if (pr->batch < 1) fail(MRF_EINVAL, "batch must be >= 1");
+  if (pr->height != topo->host.height() || pr->width != topo->host.width())
+    fail(MRF_EINVAL, "problem grid does not match topology");
+  if (pr->labels < 1 || pr->labels > 256) fail(MRF_EINVAL, "label count must be in [1, 256]");
+  if (!pr->unary || !pr->pairwise) fail(MRF_EINVAL, "null unary or pairwise");
+  if (!pr->weight_planes && !(pr->weight >= 0.0f)) fail(MRF_EINVAL, "edge weight must be nonnegative");
+}
+
+void validate_rho(const mrf_problem_f32* pr) {
+  if (!pr->rho_planes && !(pr->rho > 0.0f && pr->rho <= 1.0f)) fail(MRF_EINVAL, "rho must be in (0, 1]");
+}
+
+Geometry make_geometry(mrf_topology_t topo, const mrf_problem_f32* pr, int K_cap) {
+  Geometry g{};
+  g.N = topo->host.nodes();
+  g.L = pr->labels;
+  g.R = topo->host.num_dirs();
+  g.W = topo->host.width();
+  g.K_cap = K_cap;
+  g.E = topo->host.total_edges();
+  for (int r = 0; r < g.R; ++r) {
+    g.dir_offset[r] = topo->host.dir_offset(r);
+    g.node_step[r] = topo->host.node_step(r);
+  }
+  return g;
+}
+
+Potentials make_potentials(const mrf_problem_f32* pr) {
+  return Potentials{pr->unary, pr->pairwise, pr->weight, pr->weight_planes, pr->rho, pr->rho_planes};
+}
+
+size_t messages_bytes(mrf_topology_t topo, const mrf_problem_f32* pr) {
+  return sizeof(float) * size_t(pr->batch) * topo->host.num_dirs() * topo->host.nodes() * pr->labels;
+}
+
+int threads_for(int L) { return std::min(256, (L + 31) / 32 * 32); }
+
+struct FwdLaunch {
+  int table_mode;
+  size_t smem;
+};
+
+FwdLaunch plan_forward(const mrf_problem_f32* pr) {
+  const int L = pr->labels;
+  const size_t head = sizeof(float) * (256 + 16);
+  const size_t tab = sizeof(float) * size_t(L) * L;
+  if (head + tab <= 200 * 1024) return {pr->weight_planes ? int(kTabV) : int(kTabWV), head + tab};
+  return {int(kTabGlobal), head};
+}
+
+template <bool TRWP>
+void launch_forward_sweep(mrf_topology_t topo, const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines,
+                          int nlines, const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k,
+                          cudaStream_t stream) {
+  if (nlines == 0) return;
+  const FwdLaunch pl = plan_forward(pr);
+  auto kern = fwd_dense_kernel<TRWP>;
+  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
+             "cudaFuncSetAttribute");
+  dim3 grid(std::min(nlines, 65535), pr->batch);
+  kern<<<grid, threads_for(pr->labels), pl.smem, stream>>>(g, make_potentials(pr), lines, nlines, m_in, m_out, p, q,
+                                                           k, pl.table_mode);
+  cuda_check(cudaGetLastError(), "fwd_dense_kernel launch");
+}
+
+void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* messages, float* cost, uint16_t* labels,
+                      cudaStream_t stream) {
+  if (!cost && !labels) return;
+  const int64_t warps = int64_t(pr->batch) * N;
+  const int per_block = 8;
+  const int64_t blocks = (warps + per_block - 1) / per_block;
+  aggregate_kernel<<<unsigned(blocks), per_block * 32, 0, stream>>>(pr->batch, N, pr->labels, R, pr->unary, messages,
+                                                                    cost, labels);
+  cuda_check(cudaGetLastError(), "aggregate_kernel launch");
+}
+
+void isgmr_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap, const float* m_in, float* m_out,
+                uint8_t* p, uint8_t* q, cudaStream_t stream) {
+  const Geometry g = make_geometry(topo, pr, K_cap);
+  const LineDesc* lines = topo->device_lines();
+  launch_forward_sweep<false>(topo, pr, g, lines, int(topo->all_lines.size()), m_in, m_out, p, q, k, stream);
+}
+
+void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap, float* m, uint8_t* p, uint8_t* q,
+               cudaStream_t stream) {
+  const Geometry g = make_geometry(topo, pr, K_cap);
+  const LineDesc* lines = topo->device_lines();
+  for (int r = 0; r < g.R; ++r)  // directions strictly sequential (trwp.hpp:50)
+    launch_forward_sweep<true>(topo, pr, g, lines + topo->dir_start[r], int(topo->dir_lines[r].size()), m, m, p, q,
+                               k, stream);
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+size_t vslot_bytes(mrf_topology_t topo, const mrf_problem_f32* pr) {
+  return sizeof(float) * size_t(pr->batch) * kBwdSlots * 2 * pr->labels * pr->labels;
+}
+
+template <bool TRWP>
+void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const uint8_t* p, const uint8_t* q,
+                  const float* grad_cost, const mrf_grads_f32* grads, void* ws, size_t ws_bytes,
+                  cudaStream_t stream) {
+  const int R = topo->host.num_dirs(), N = topo->host.nodes(), L = pr->labels, B = pr->batch;
+  const size_t mb = messages_bytes(topo, pr), vb = vslot_bytes(topo, pr);
+  const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb);
+  if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
+  char* w = static_cast<char*>(ws);
+  float* gm = reinterpret_cast<float*>(w);
+  float* gnext = TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb));
+  float* vslots = reinterpret_cast<float*>(w + align_up(mb) * (TRWP ? 1 : 2));
+  const size_t NL = size_t(N) * L;
+
+  // make_gradients (autodiff.hpp:33-44) and gm <- dc for every r (:72-74)
+  cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
+             "copy grad_cost");
+  if (grads->weight_planes)
+    cuda_check(cudaMemsetAsync(grads->weight_planes, 0, sizeof(float) * B * (R / 2) * N, stream), "zero dw");
+  cuda_check(cudaMemsetAsync(vslots, 0, vb, stream), "zero dV slots");
+  {
+    const int64_t total = int64_t(B) * R * NL;
+    broadcast_planes_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, R, int64_t(NL), grad_cost, gm);
+    cuda_check(cudaGetLastError(), "broadcast launch");
+  }
+  if (!TRWP) cuda_check(cudaMemsetAsync(gnext, 0, mb, stream), "zero gm_next");
+
+  const Geometry g = make_geometry(topo, pr, K);
+  const Potentials pot = make_potentials(pr);
+  const LineDesc* lines = topo->device_lines();
+  const int nt = threads_for(L);
+  for (int k = K - 1; k >= 0; --k) {
+    for (int ri = 0; ri < R; ++ri) {
+      const int r = TRWP ? R - 1 - ri : ri;
+      const int nl = int(topo->dir_lines[r].size());
+      if (nl > 0) {
+        dim3 grid(std::min(nl, kBwdSlots), B);
+        // every image uses kBwdSlots slot columns; CTAs beyond nl never exist,
+        // their slots stay zero.
+        bwd_dense_kernel<TRWP><<<grid, nt, 0, stream>>>(g, pot, lines + topo->dir_start[r], nl, r, p, q, k, gm, gnext,
+                                                        grads->unary, grads->weight_planes, vslots, kBwdSlots);
+        cuda_check(cudaGetLastError(), "bwd_dense_kernel launch");
+      }
+      if (TRWP)  // plane r consumed (autodiff.hpp:190-193)
+        cuda_check(cudaMemset2DAsync(gm + size_t(r) * NL, sizeof(float) * R * NL, 0, sizeof(float) * NL, B, stream),
+                   "zero plane");
+    }
+    if (!TRWP) {  // swap and clear (autodiff.hpp:122-123)
+      std::swap(gm, gnext);
+      if (k > 0) cuda_check(cudaMemsetAsync(gnext, 0, mb, stream), "zero gm_next");
+    }
+  }
+  if (grads->pairwise) {
+    const int64_t total = int64_t(B) * L * L;
+    reduce_vslots_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, kBwdSlots, L, vslots, grads->pairwise);
+    cuda_check(cudaGetLastError(), "reduce_vslots launch");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mrf_last_error(void) { return g_last_error.c_str(); }
+int mrf_version(void) { return 100; }
+
+int mrf_topology_create(int height, int width, int connectivity, mrf_topology_t* out) {
+  return guarded([&] {
+    if (!out) fail(MRF_EINVAL, "null out");
+    *out = new mrf_topology_s(height, width, connectivity);
+  });
+}
+
+int mrf_topology_destroy(mrf_topology_t topo) {
+  return guarded([&] { delete topo; });
+}
+
+int mrf_topology_info(mrf_topology_t topo, int* num_dirs, int64_t* total_edges, int64_t* edge_count,
+                      int64_t* dir_offset) {
+  return guarded([&] {
+    if (!topo) fail(MRF_EINVAL, "null topology");
+    if (num_dirs) *num_dirs = topo->host.num_dirs();
+    if (total_edges) *total_edges = topo->host.total_edges();
+    for (int r = 0; r < topo->host.num_dirs(); ++r) {
+      if (edge_count) edge_count[r] = topo->host.edge_count(r);
+      if (dir_offset) dir_offset[r] = topo->host.dir_offset(r);
+    }
+  });
+}
+
+int mrf_topology_edge_index(mrf_topology_t topo, int32_t* out) {
+  return guarded([&] {
+    if (!topo || !out) fail(MRF_EINVAL, "null argument");
+    const auto v = topo->host.edge_index();
+    std::memcpy(out, v.data(), sizeof(int32_t) * v.size());
+  });
+}
+
+int mrf_topology_scanlines(mrf_topology_t topo, int r, int32_t* first, int32_t* length, int32_t* count, int cap) {
+  return guarded([&] {
+    if (!topo || r < 0 || r >= topo->host.num_dirs()) fail(MRF_EINVAL, "bad topology or direction");
+    const auto& ls = topo->host.lines(r);
+    if (count) *count = int32_t(ls.size());
+    for (int t = 0; t < int(ls.size()) && t < cap; ++t) {
+      if (first) first[t] = ls[t].first;
+      if (length) length[t] = ls[t].length;
+    }
+  });
+}
+
+int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaStream_t stream);
+
+size_t mrf_forward_workspace_bytes(mrf_topology_t topo, const mrf_problem_f32* prob, int engine, int iterations) {
+  (void)iterations;
+  if (!topo || !prob) return 0;
+  return engine == MRF_ENGINE_ISGMR ? align_up(messages_bytes(topo, prob)) : 0;
+}
+
+int mrf_isgmr_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const mrf_forward_out* out,
+                          void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (iterations < 1) fail(MRF_EINVAL, "isgmr_forward: iterations must be >= 1");
+    if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
+    const size_t mb = messages_bytes(topo, prob);
+    if (!workspace || workspace_bytes < mb) fail(MRF_EINVAL, "forward workspace too small");
+    float* bufs[2] = {out->messages, static_cast<float*>(workspace)};
+    cuda_check(cudaMemsetAsync(bufs[0], 0, mb, stream), "zero m");
+    cuda_check(cudaMemsetAsync(bufs[1], 0, mb, stream), "zero mhat");
+    // Iteration k writes bufs[(K-1-k)&1] so the last one lands in out->messages;
+    // the publish m <- mhat (isgmr.hpp:55) is the buffer swap.
+    for (int k = 0; k < iterations; ++k) {
+      float* dst = bufs[(iterations - 1 - k) & 1];
+      const float* src = bufs[(iterations - k) & 1];
+      isgmr_step(topo, prob, k, iterations, src, dst, out->p, out->q, stream);
+    }
+    launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
+  });
+}
+
+int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const mrf_forward_out* out,
+                         void* workspace, size_t workspace_bytes, cudaStream_t stream) {
+  (void)workspace;
+  (void)workspace_bytes;
+  return guarded([&] {
+    validate_problem(topo, prob);
+    validate_rho(prob);
+    if (iterations < 1) fail(MRF_EINVAL, "trwp_forward: iterations must be >= 1");
+    if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
+    cuda_check(cudaMemsetAsync(out->messages, 0, messages_bytes(topo, prob), stream), "zero m");
+    for (int k = 0; k < iterations; ++k) trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, stream);
+    launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
+  });
+}
+
+int mrf_isgmr_step_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int k, int K_cap, const float* m_in,
+                       float* m_out, uint8_t* p, uint8_t* q, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (k < 0 || k >= K_cap) fail(MRF_EINVAL, "iteration index out of range");
+    if (!m_in || !m_out || !p || !q || m_in == m_out) fail(MRF_EINVAL, "bad step buffers");
+    isgmr_step(topo, prob, k, K_cap, m_in, m_out, p, q, stream);
+  });
+}
+
+int mrf_trwp_step_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int k, int K_cap, float* messages, uint8_t* p,
+                      uint8_t* q, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    validate_rho(prob);
+    if (k < 0 || k >= K_cap) fail(MRF_EINVAL, "iteration index out of range");
+    if (!messages || !p || !q) fail(MRF_EINVAL, "bad step buffers");
+    trwp_step(topo, prob, k, K_cap, messages, p, q, stream);
+  });
+}
+
+int mrf_aggregate_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const float* messages, float* cost,
+                      uint16_t* labels, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (!messages) fail(MRF_EINVAL, "null messages");
+    launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), messages, cost, labels, stream);
+  });
+}
+
+size_t mrf_backward_workspace_bytes(mrf_topology_t topo, const mrf_problem_f32* prob, int engine, int iterations) {
+  (void)iterations;
+  if (!topo || !prob) return 0;
+  const size_t mb = align_up(messages_bytes(topo, prob));
+  return mb * (engine == MRF_ENGINE_ISGMR ? 2 : 1) + align_up(vslot_bytes(topo, prob));
+}
+
+int mrf_isgmr_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const uint8_t* p,
+                           const uint8_t* q, const float* grad_cost, const mrf_grads_f32* grads, void* workspace,
+                           size_t workspace_bytes, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (iterations < 1) fail(MRF_EINVAL, "backward: iterations must be >= 1");
+    if (!p || !q || !grad_cost || !grads || !grads->unary) fail(MRF_EINVAL, "null backward argument");
+    run_backward<false>(topo, prob, iterations, p, q, grad_cost, grads, workspace, workspace_bytes, stream);
+  });
+}
+
+int mrf_trwp_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const uint8_t* p,
+                          const uint8_t* q, const float* grad_cost, const mrf_grads_f32* grads, void* workspace,
+                          size_t workspace_bytes, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    validate_rho(prob);
+    if (iterations < 1) fail(MRF_EINVAL, "backward: iterations must be >= 1");
+    if (!p || !q || !grad_cost || !grads || !grads->unary) fail(MRF_EINVAL, "null backward argument");
+    run_backward<true>(topo, prob, iterations, p, q, grad_cost, grads, workspace, workspace_bytes, stream);
+  });
+}
+
+}  // extern "C"

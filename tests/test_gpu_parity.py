@@ -1,0 +1,192 @@
+"""GPU parity: libmrf_cuda.so (through the C-ABI) against the CPU checkers.
+
+Forward outputs (messages, cost, labels, p, q) must be bit-identical to the
+reference; gradients within GRAD_RTOL (1e-5, normwise) of the reference's
+float backward. Mirrors the reference's bit-identity tests
+(test_isgmr.cpp:84-96, test_trwp.cpp:73-86, test_autodiff.cpp:86-110) with
+"GPU == CPU reference" in place of "1 thread == N threads".
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_1910_10892_b200 import api
+from paper_1910_10892_b200 import workloads as WL
+from tests.gpu_util import (assert_forward_equal, assert_grads_close, gpu_backward, gpu_forward, to_mrf)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
+def test_golden_fixtures(path):
+    from tests.golden.make_golden import load
+
+    eng, pr, K, z = load(path)
+    mrf = to_mrf(pr)
+    f = gpu_forward(eng, mrf, K)
+    assert_forward_equal(f, {k: z[k] for k in ("cost", "labels", "messages", "p", "q")})
+    g = gpu_backward(eng, mrf, f, z["grad_cost"])
+    assert_grads_close(g, {k: z[k] for k in ("g_unary", "g_pairwise", "g_wplanes")})
+
+
+CASES = [
+    # H, W, L, conn, K, per_edge, explicit
+    (7, 9, 5, 4, 3, True, True),
+    (7, 9, 5, 8, 3, True, True),
+    (6, 6, 4, 16, 2, False, True),
+    (13, 11, 16, 4, 2, False, False),
+    (9, 14, 21, 8, 2, True, True),
+    (3, 17, 1, 4, 3, False, True),
+    (1, 12, 5, 4, 1, False, True),
+    (12, 1, 7, 8, 2, True, False),
+    (10, 12, 32, 4, 2, False, True),
+    (8, 9, 33, 4, 2, True, True),
+    (6, 10, 64, 8, 2, False, False),
+    (5, 7, 128, 4, 2, True, True),
+    (6, 5, 192, 4, 2, False, False),
+    (4, 6, 256, 4, 2, False, False),
+    (4, 5, 256, 8, 1, True, True),
+]
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}L{c[2]}c{c[3]}" for c in CASES])
+def test_random_problems_bit_exact(engine, case):
+    H, W, L, conn, K, per_edge, explicit = case
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=H * 1000 + W * 10 + L, per_edge=per_edge,
+                                          explicit=explicit)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    mrf = to_mrf(pr)
+    f = gpu_forward(engine, mrf, K)
+    assert_forward_equal(f, ref)
+    rng = np.random.default_rng(L)
+    _, _, gc = O.soft_head(ref.cost, rng.uniform(0.25, max(L - 1.25, 0.3), H * W), L)
+    gref = O.backward(engine, pr, K, ref.p, ref.q, gc)
+    g = gpu_backward(engine, mrf, f, gc)
+    assert_grads_close(g, gref)
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+def test_batch_images_independent(engine):
+    H, W, L, conn, K, B = 11, 9, 21, 4, 2, 3
+    uns, pls, rhos, refs = [], [], [], []
+    V = None
+    for b in range(B):
+        un, V0, wc, planes = WL.random_problem(H, W, L, conn, seed=50 + b, per_edge=True)
+        V = V0 if V is None else V
+        rho = np.random.default_rng(b).uniform(0.2, 1.0, (conn // 2) * H * W).astype(np.float32)
+        uns.append(un)
+        pls.append(planes)
+        rhos.append(rho)
+        refs.append(O.Problem(H, W, L, conn, un, V, 1.0, planes, 0.5, rho))
+    mrf = to_mrf(refs[0], batch_unary=uns, batch_wplanes=pls, batch_rho=rhos if engine == "trwp" else None)
+    f = gpu_forward(engine, mrf, K)
+    gcs = np.random.default_rng(9).normal(size=(B, H * W * L)).astype(np.float32)
+    g = gpu_backward(engine, mrf, f, gcs)
+    for b in range(B):
+        pr = refs[b] if engine == "trwp" else O.Problem(H, W, L, conn, uns[b], V, 1.0, pls[b], 0.5, None)
+        ref = O.forward(engine, pr, K)
+        assert_forward_equal(f, ref, b=b)
+        gref = O.backward(engine, pr, K, ref.p, ref.q, gcs[b])
+        assert_grads_close(g, gref, b=b)
+    # shared-parameter pack: sum over the batch of dV, and the total dw
+    packed = api.pack_shared_grads(mrf, g).cpu().numpy()
+    want = g.pairwise.sum(0).reshape(-1).cpu().numpy()
+    assert np.allclose(packed[:-1], want, rtol=1e-5, atol=1e-6)
+    assert np.isclose(packed[-1], g.edge_weights.sum().item(), rtol=1e-4)
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+def test_engine_step_api_matches_forward(engine):
+    H, W, L, conn, K = 9, 10, 8, 8, 3
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=77)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    mrf = to_mrf(pr)
+    eng = (api.IsgmrEngine if engine == "isgmr" else api.TrwpEngine)(mrf, K)
+    ref_msgs = []
+    for k in range(K):
+        eng.step()
+        ref_msgs.append(O.forward(engine, pr, k + 1))
+        cost, labels = eng.aggregate()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits_(eng.messages()[0]), bits_(ref_msgs[-1].messages))
+        assert np.array_equal(bits_(cost[0]), bits_(ref_msgs[-1].cost))
+        assert np.array_equal(labels[0].cpu().numpy().view(np.uint16), ref_msgs[-1].labels)
+    assert np.array_equal(eng.p[0].cpu().numpy().reshape(-1), ref_msgs[-1].p)
+    assert np.array_equal(eng.q[0].cpu().numpy().reshape(-1), ref_msgs[-1].q)
+
+
+def bits_(t):
+    return t.cpu().numpy().reshape(-1).view(np.uint8)
+
+
+def test_zero_cost_gradient_gives_zero_gradients():
+    """test_autodiff.cpp:44-54."""
+    H, W, L, conn, K = 6, 6, 4, 4, 2
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=1, per_edge=True)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    mrf = to_mrf(pr)
+    for engine in ("isgmr", "trwp"):
+        f = gpu_forward(engine, mrf, K)
+        g = gpu_backward(engine, mrf, f, np.zeros(H * W * L, np.float32))
+        assert not g.unary.any() and not g.pairwise.any() and not g.edge_weights.any()
+
+
+def test_backward_deterministic_run_to_run():
+    H, W, L, conn, K = 12, 13, 16, 8, 2
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=5, per_edge=True)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    mrf = to_mrf(pr)
+    gc = np.random.default_rng(3).normal(size=H * W * L).astype(np.float32)
+    for engine in ("isgmr", "trwp"):
+        f = gpu_forward(engine, mrf, K)
+        a = gpu_backward(engine, mrf, f, gc)
+        b = gpu_backward(engine, mrf, f, gc)
+        for x, y in ((a.unary, b.unary), (a.pairwise, b.pairwise), (a.edge_weights, b.edge_weights)):
+            assert torch.equal(x, y)
+
+
+def test_invalid_arguments_raise():
+    H, W, L, conn = 4, 4, 3, 4
+    un, V, wc, _ = WL.random_problem(H, W, L, conn, seed=2)
+    mrf = to_mrf(O.Problem(H, W, L, conn, un, V, wc, None, 0.5, None))
+    with pytest.raises(ValueError):
+        api.isgmr_forward(mrf, 0)
+    bad = api.MRF(mrf.topo, mrf.unary, mrf.V, 1.0, 1.5)
+    with pytest.raises(ValueError):
+        api.trwp_forward(bad, 1)
+    x = mrf.unary.clone()
+    assert api.check_finite(x)
+    x[0, 3, 1] = float("inf")
+    assert not api.check_finite(x)
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+def test_c1_full_size_matches_reference(engine):
+    """Config C1 (288x384, L=16, 4 dirs, K=5, TL tau=2) at full size against
+    the reference library itself (oracle/_ref, all host threads)."""
+    if not O.have_ref():
+        pytest.skip("reference library not present")
+    wl = WL.config("C1")
+    pr = O.Problem(wl.H, wl.W, wl.L, wl.conn, wl.unary[0], wl.V, wl.w_const, None, 0.5, None)
+    ref = O.forward(engine, pr, wl.K, impl="ref", threads=0)
+    mrf = to_mrf(pr)
+    f = gpu_forward(engine, mrf, wl.K)
+    assert_forward_equal(f, ref)
+    gc = np.full(wl.N * wl.L, 1.0 / (wl.N * wl.L), np.float32)
+    gref = O.backward(engine, pr, wl.K, ref.p, ref.q, gc, impl="ref", threads=0)
+    g = gpu_backward(engine, mrf, f, gc)
+    assert_grads_close(g, gref)
