@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Benchmark: ISGMR / TRWP min-sum message passing, fwd+bwd, on B200.
+
+Workload (BASELINE.json configs[1]): C2 = TRWP, 4 directions,
+K=5 iterations, KITTI-shaped 375x1242 synthetic stereo cost volume, L=192,
+truncated-linear pairwise (tau=2), w=1, rho=0.5; one image per GPU (weak
+scaling: images shard across GPUs, one NCCL all-reduce of the shared pairwise
+gradient per step when N > 1). A "step" = forward (K iterations, indices
+stored) + aggregate + index-driven backward for dc = 1/(N*L) (acceptance.cpp
+:282-283) + shared-gradient pack (+ all-reduce).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C1..C5]
+
+Prints ONE JSON line on rank 0. `value` = whole-job G label-updates/s
+(LU = K * sum_r|E^r| * L per image) with inputs resident in HBM; `e2e` = the
+same metric through the C-ABI with host (pinned) buffers, H2D/D2H inside the
+timed region; `roofline` = the dominant kernel class measured with CUDA events
+on its launch stream inside the timed region; `cpu_baseline` = the reference
+library (oracle/_ref, compiled from the reference sources) timed on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Peaks: MEASURED_PEAKS.json (driver-written) for HBM; the FP32 ALU roof is the
+# nominal P_cand of SURVEY.md §8d (148 SMs x 128 lanes x 2 flop x 1.965 GHz).
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FALLBACK_HBM_GBS = 6650.0
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+# --------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workloads
+
+def make_workload(cfg: str, rank: int):
+    from paper_1910_10892_b200 import workloads as WL
+
+    wl = WL.config(cfg)
+    if rank and wl.name in ("C1", "C2", "C3"):
+        # a different image per rank (weak scaling over independent images)
+        seed = {"C1": 1, "C2": 2, "C3": 3}[wl.name] + 1000 * rank
+        wl.unary = WL.stereo_like(wl.H, wl.W, wl.L, seed)[None]
+    return wl
+
+
+def algorithmic_units(wl, E, E_r):
+    """Per-image work: label-updates, candidates, and the
+    forward / backward algorithmic bytes."""
+    K, L, R, N = wl.K, wl.L, wl.conn, wl.N
+    per_edge = wl.w_planes is not None
+    LU = K * E * L
+    cand = LU * L
+    P = R if wl.engine == "isgmr" else R + 1
+    X = R - 2 if wl.engine == "isgmr" else R - 1
+    fwd_bytes = K * E * (4 * L * P + L + 1 + (4 if per_edge else 0)) + (R + 2) * N * L * 4 + 2 * N
+    bwd_bytes = K * E * (13 * L + 8 * L * X + 9) + (K + 1) * R * N * L * 4 + N * L * 4
+    return LU, cand, fwd_bytes, bwd_bytes
+
+
+# ---------------------------------------------------------------- cpu baseline
+
+def cpu_reference_sample(wl, budget_s: float = 12.0, rows: int | None = None):
+    """Reference library (oracle/_ref; restatement if absent) fwd+bwd on a
+    horizontal strip of the same workload, all host threads. Returns
+    (LU/s, seconds, sample description, kind, cores)."""
+    from oracle import oracle as O
+
+    kind = "reference" if O.have_ref() else "port"
+    impl = "ref" if kind == "reference" else "oracle"
+    cores = os.cpu_count() if kind == "reference" else 1
+    K = 1  # one of the K identical iterations; LU scales linearly in K
+
+    def run(h):
+        un = wl.unary[0].reshape(wl.H, wl.W * wl.L)[:h].reshape(-1).copy()
+        wp = None
+        if wl.w_planes is not None:
+            wp = wl.w_planes[0].reshape(wl.conn // 2, wl.H, wl.W)[:, :h].reshape(-1).copy()
+        pr = O.Problem(h, wl.W, wl.L, wl.conn, un, wl.V, wl.w_const, wp, wl.rho_const, None)
+        E = O.total_edges(h, wl.W, wl.conn)
+        gc = np.full(h * wl.W * wl.L, 1.0 / (h * wl.W * wl.L), np.float32)
+        t0 = time.perf_counter()
+        f = O.forward(wl.engine, pr, K, impl=impl, threads=0)
+        O.backward(wl.engine, pr, K, f.p, f.q, gc, impl=impl, threads=0)
+        dt = time.perf_counter() - t0
+        return K * E * wl.L, dt
+
+    if rows is None:
+        lu, dt = run(min(8, wl.H))
+        rows = int(min(wl.H, max(2, 8 * budget_s / max(dt, 1e-3))))
+    lu, dt = run(rows)
+    desc = (f"{wl.name} {wl.engine.upper()}-{wl.conn} strip rows[0:{rows}] x {wl.W}, L={wl.L}, K=1 of {wl.K} "
+            f"(per-iteration work identical), fwd+bwd, OpenMP threads={cores}")
+    return lu / dt, dt, desc, kind, cores, rows
+
+
+# --------------------------------------------------------------------- runs
+
+def run_reference_arm(args, wl):
+    """--impl reference: the reference CPU implementation on the host cores."""
+    total_steps = args.steps + args.warmup
+    budget = max(2.0, 150.0 / max(total_steps, 1))
+    _, _, desc, kind, cores, rows = cpu_reference_sample(wl, budget_s=budget)
+    lus, dts = [], []
+    for i in range(total_steps):
+        lu_s, dt, desc, kind, cores, rows = cpu_reference_sample(wl, rows=rows)
+        if i >= args.warmup:
+            lus.append(lu_s * dt)
+            dts.append(dt)
+    value = sum(lus) / sum(dts) / 1e9
+    line = {
+        "impl": "reference", "metric": metric_name(wl), "value": value, "unit": "G label-updates/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(dts) / len(dts), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(wl, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "G label-updates/s", "cores": cores, "kind": kind,
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "G label-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(wl):
+    return (f"fwd+bwd G label-updates/s, {wl.engine.upper()}-{wl.conn} {wl.W}x{wl.H}x{wl.L} K={wl.K} "
+            f"(ms/image alongside)")
+
+
+def config_dict(wl, n):
+    return {"workload": f"{wl.name}: {wl.engine.upper()} fwd+bwd, {wl.conn} directions, K={wl.K}, "
+                        f"{wl.W}x{wl.H} synthetic volume, {wl.L} labels",
+            "H": wl.H, "W": wl.W, "L": wl.L, "K": wl.K, "connectivity": wl.conn, "engine": wl.engine,
+            "images_per_gpu": wl.B, "global_batch": wl.B * n, "parallelism": f"dp{n}",
+            "l2": "inputs larger than L2 (unary, messages and indices each exceed 126 MB per image)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args, make_workload(args.config, 0))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_10892_b200 import _lib, api
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.lib()  # fail loudly if the CUDA library is missing
+
+    wl = make_workload(args.config, rank)
+    topo = api.GridTopology(wl.H, wl.W, wl.conn)
+    E = topo.total_edges
+    E_r = topo.edge_count
+    B = wl.B
+    unary = torch.from_numpy(wl.unary.reshape(B, wl.N, wl.L)).to(dev)
+    V = torch.from_numpy(wl.V.reshape(wl.L, wl.L)).to(dev)
+    w = wl.w_const
+    if wl.w_planes is not None:
+        w = torch.from_numpy(wl.w_planes.reshape(B, wl.conn // 2, wl.N)).to(dev)
+    mrf = api.MRF(topo, unary, V, w, wl.rho_const)
+    gc = torch.full_like(unary, 1.0 / (wl.N * wl.L))
+    fwd_fn = api.isgmr_forward if wl.engine == "isgmr" else api.trwp_forward
+    bwd_fn = api.isgmr_backward if wl.engine == "isgmr" else api.trwp_backward
+    fwd_out = api._alloc_forward(mrf, wl.K)
+    grads = api.GradientSet(torch.empty_like(unary), torch.empty((B, wl.L, wl.L), device=dev),
+                            torch.empty((B, wl.conn // 2, wl.N), device=dev))
+    shared = torch.empty(wl.L * wl.L + 1, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        f = fwd_fn(mrf, wl.K, out=fwd_out)
+        bwd_fn(mrf, f, gc, out=grads)
+        api.pack_shared_grads(mrf, grads, out=shared)
+        if world > 1:
+            dist.all_reduce(shared)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    _lib.check(_lib.lib().mrf_profiler_enable(1))
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    prof = {}
+    import ctypes as C
+    for cls in range(4):
+        tot = C.c_double()
+        n = C.c_int64()
+        _lib.check(_lib.lib().mrf_profiler_read(cls, C.byref(tot), C.byref(n)))
+        prof[cls] = (tot.value, n.value)
+    _lib.check(_lib.lib().mrf_profiler_enable(0))
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    LU, cand, fwd_bytes, bwd_bytes = algorithmic_units(wl, E, E_r)
+    images = B * world * args.steps
+    value = LU * images / (ms / 1e3) / 1e9
+    ms_per_step = ms / args.steps
+
+    # ---- roofline of the dominant kernel class (device time inside the timed region)
+    hbm_peak, peak_kind = load_peaks()
+    fwd_ms, fwd_n = prof[_lib.KCLASS_FWD_SWEEP]
+    bwd_ms, bwd_n = prof[_lib.KCLASS_BWD_SWEEP]
+    n_img_local = B * args.steps
+    if fwd_ms >= bwd_ms:
+        achieved = 2.0 * cand * n_img_local / (fwd_ms / 1e3) / 1e12
+        roof = {"kernel": "fwd sweep (min-plus + argmin)", "bound": "fp32_alu", "achieved": achieved,
+                "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP32_PEAK_TFLOPS,
+                "peak_source": "nominal P_cand = 148 SM x 128 lanes x 2 flop x 1.965 GHz (SURVEY.md §8d)",
+                "work_per_launch": f"2 flop x E_r x L^2 candidates (avg over {fwd_n} launches)",
+                "avg_launch_ms": fwd_ms / max(fwd_n, 1), "share_of_step": fwd_ms / max(ms, 1e-9)}
+    else:
+        achieved = bwd_bytes * n_img_local / (bwd_ms / 1e3) / 1e9
+        roof = {"kernel": "bwd sweep (index-driven scatter)", "bound": "hbm", "achieved": achieved,
+                "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_kind,
+                "avg_launch_ms": bwd_ms / max(bwd_n, 1), "share_of_step": bwd_ms / max(ms, 1e-9)}
+    roof["traffic"] = ncu_traffic(wl.name, roof["kernel"])
+    roof["fwd_ms_per_image"] = fwd_ms / n_img_local
+    roof["bwd_ms_per_image"] = bwd_ms / n_img_local
+    roof["fwd_alu_frac"] = (2.0 * cand * n_img_local / (fwd_ms / 1e3) / 1e12) / FP32_PEAK_TFLOPS if fwd_ms else None
+    roof["bwd_hbm_frac"] = (bwd_bytes * n_img_local / (bwd_ms / 1e3) / 1e9) / hbm_peak if bwd_ms else None
+    launches = sum(n for _, n in prof.values())
+
+    # ---- end to end through the C-ABI with pinned host buffers
+    e2e = run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, LU, barrier)
+
+    line = {
+        "metric": metric_name(wl), "value": value, "unit": "G label-updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_image": ms / images * world, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded stereo-like cost volume; no datasets)",
+        "config": config_dict(wl, world), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        lu_s, dt, desc, kind, cores, _ = cpu_reference_sample(wl)
+        line["cpu_baseline"] = {"value": lu_s / 1e9, "unit": "G label-updates/s", "cores": cores, "kind": kind,
+                                "sample": desc, "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, LU, barrier):
+    """Same step through the C-ABI, inputs from pinned host memory and the
+    step's result (gradients + labels) read back to the host, inside the
+    timed region."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_10892_b200 import api
+
+    h_unary = mrf.unary.cpu().pin_memory()
+    h_gc = torch.full(tuple(mrf.unary.shape), 1.0 / (wl.N * wl.L)).pin_memory()
+    h_gu = torch.empty_like(h_unary).pin_memory()
+    h_gv = torch.empty(tuple(grads.pairwise.shape)).pin_memory()
+    h_gw = torch.empty(tuple(grads.edge_weights.shape)).pin_memory()
+    h_lab = torch.empty(tuple(fwd_out.labels.shape), dtype=torch.int16).pin_memory()
+    d_gc = torch.empty_like(mrf.unary)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        mrf.unary.copy_(h_unary, non_blocking=True)
+        d_gc.copy_(h_gc, non_blocking=True)
+        f = fwd_fn(mrf, wl.K, out=fwd_out)
+        bwd_fn(mrf, f, d_gc, out=grads)
+        api.pack_shared_grads(mrf, grads, out=shared)
+        if world > 1:
+            dist.all_reduce(shared)
+        h_gu.copy_(grads.unary, non_blocking=True)
+        h_gv.copy_(grads.pairwise, non_blocking=True)
+        h_gw.copy_(grads.edge_weights, non_blocking=True)
+        h_lab.copy_(fwd_out.labels, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    images = wl.B * world * args.e2e_steps
+    h2d = h_unary.numel() * 4 + h_gc.numel() * 4
+    d2h = (h_gu.numel() + h_gv.numel() + h_gw.numel()) * 4 + h_lab.numel() * 2
+    return {"value": LU * images / (ms / 1e3) / 1e9, "unit": "G label-updates/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms / args.e2e_steps,
+            "path": "C-ABI mrf_*_forward_f32 + mrf_*_backward_f32 with pinned host inputs/outputs"}
+
+
+def ncu_traffic(cfg, kernel):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/ncu_full_<cfg>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_full_{cfg}.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        key = "fwd" if kernel.startswith("fwd") else "bwd"
+        return d[key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

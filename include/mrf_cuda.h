@@ -168,6 +168,22 @@ int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const m
  * per training step, over the buffer mrf_pack_shared_grads_f32 produced. */
 int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream);
 
+/* ---------------------------------------------------------- instrumentation */
+
+/* Kernel classes for the launch profiler. */
+#define MRF_KCLASS_FWD_SWEEP 0
+#define MRF_KCLASS_BWD_SWEEP 1
+#define MRF_KCLASS_AGGREGATE 2
+#define MRF_KCLASS_AUX 3
+#define MRF_KCLASS_COUNT 4
+
+/* Not part of the reference surface. When enabled (on != 0; clears previous
+ * records), every kernel launch of this library is bracketed by CUDA events
+ * recorded on its own stream. mrf_profiler_read synchronises those events and
+ * returns the summed device time and launch count of one kernel class. */
+int mrf_profiler_enable(int on);
+int mrf_profiler_read(int kernel_class, double* total_ms, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,7 +64,10 @@ SIGNATURES = {
     "mrf_trwp_backward_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _GR, _vp, _sz, _vp]),
     "mrf_pack_shared_grads_f32": (_i, [_PP, _i, _GR, _vp, _vp]),
     "mrf_allreduce_grads_f32": (_i, [_vp, _vp, _sz, _vp]),
+    "mrf_profiler_enable": (_i, [_i]),
+    "mrf_profiler_read": (_i, [_i, C.POINTER(C.c_double), _i64p]),
 }
+KCLASS_FWD_SWEEP, KCLASS_BWD_SWEEP, KCLASS_AGGREGATE, KCLASS_AUX = 0, 1, 2, 3
 
 _lib = None
 

@@ -59,6 +59,61 @@ int guarded(F&& f) {
 
 constexpr int kBwdSlots = 592;  // 4 x 148 SMs: persistent backward CTAs per image
 
+// Optional launch instrumentation: when enabled, every kernel launch is
+// bracketed by CUDA events recorded on its own stream, so callers can read
+// per-kernel-class device time for a region (bench.py's roofline).
+struct Profiler {
+  struct Rec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::mutex mu;
+  bool on = false;
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+
+  cudaEvent_t take() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void recycle() {
+    for (auto& r : recs) {
+      pool.push_back(r.a);
+      pool.push_back(r.b);
+    }
+    recs.clear();
+  }
+};
+Profiler g_prof;
+
+class ProfScope {
+ public:
+  ProfScope(cudaStream_t s, int cls) : s_(s), cls_(cls) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (!g_prof.on) return;
+    a_ = g_prof.take();
+    b_ = g_prof.take();
+    cudaEventRecord(a_, s_);
+  }
+  ~ProfScope() {
+    if (!a_) return;
+    cudaEventRecord(b_, s_);
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.recs.push_back({cls_, a_, b_});
+  }
+
+ private:
+  cudaStream_t s_;
+  int cls_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
 }  // namespace
 
 // Topology handle: host geometry plus lazily uploaded per-device line tables.
@@ -183,6 +238,7 @@ void launch_forward_sweep(mrf_topology_t topo, const mrf_problem_f32* pr, const 
   cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
              "cudaFuncSetAttribute");
   dim3 grid(std::min(nlines, 65535), pr->batch);
+  ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
   kern<<<grid, threads_for(pr->labels), pl.smem, stream>>>(g, make_potentials(pr), lines, nlines, m_in, m_out, p, q,
                                                            k, pl.table_mode);
   cuda_check(cudaGetLastError(), "fwd_dense_kernel launch");
@@ -194,6 +250,7 @@ void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* mess
   const int64_t warps = int64_t(pr->batch) * N;
   const int per_block = 8;
   const int64_t blocks = (warps + per_block - 1) / per_block;
+  ProfScope ps(stream, MRF_KCLASS_AGGREGATE);
   aggregate_kernel<<<unsigned(blocks), per_block * 32, 0, stream>>>(pr->batch, N, pr->labels, R, pr->unary, messages,
                                                                     cost, labels);
   cuda_check(cudaGetLastError(), "aggregate_kernel launch");
@@ -243,6 +300,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   cuda_check(cudaMemsetAsync(vslots, 0, vb, stream), "zero dV slots");
   {
     const int64_t total = int64_t(B) * R * NL;
+    ProfScope ps(stream, MRF_KCLASS_AUX);
     broadcast_planes_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, R, int64_t(NL), grad_cost, gm);
     cuda_check(cudaGetLastError(), "broadcast launch");
   }
@@ -260,6 +318,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
         dim3 grid(std::min(nl, kBwdSlots), B);
         // every image uses kBwdSlots slot columns; CTAs beyond nl never exist,
         // their slots stay zero.
+        ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         bwd_dense_kernel<TRWP><<<grid, nt, 0, stream>>>(g, pot, lines + topo->dir_start[r], nl, r, p, q, k, gm, gnext,
                                                         grads->unary, grads->weight_planes, vslots, kBwdSlots);
         cuda_check(cudaGetLastError(), "bwd_dense_kernel launch");
@@ -275,6 +334,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   }
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
+    ProfScope ps(stream, MRF_KCLASS_AUX);
     reduce_vslots_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, kBwdSlots, L, vslots, grads->pairwise);
     cuda_check(cudaGetLastError(), "reduce_vslots launch");
   }
@@ -433,6 +493,32 @@ int mrf_trwp_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
     if (iterations < 1) fail(MRF_EINVAL, "backward: iterations must be >= 1");
     if (!p || !q || !grad_cost || !grads || !grads->unary) fail(MRF_EINVAL, "null backward argument");
     run_backward<true>(topo, prob, iterations, p, q, grad_cost, grads, workspace, workspace_bytes, stream);
+  });
+}
+
+int mrf_profiler_enable(int on) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.recycle();
+    g_prof.on = on != 0;
+  });
+}
+
+int mrf_profiler_read(int kernel_class, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    double t = 0.0;
+    int64_t n = 0;
+    for (const auto& r : g_prof.recs) {
+      if (r.cls != kernel_class) continue;
+      cuda_check(cudaEventSynchronize(r.b), "profiler sync");
+      float ms = 0.0f;
+      cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "profiler elapsed");
+      t += ms;
+      ++n;
+    }
+    if (total_ms) *total_ms = t;
+    if (launches) *launches = n;
   });
 }
 

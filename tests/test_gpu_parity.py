@@ -130,7 +130,8 @@ def test_engine_step_api_matches_forward(engine):
 
 
 def bits_(t):
-    return t.cpu().numpy().reshape(-1).view(np.uint8)
+    a = t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+    return np.ascontiguousarray(a).reshape(-1).view(np.uint8)
 
 
 def test_zero_cost_gradient_gives_zero_gradients():
