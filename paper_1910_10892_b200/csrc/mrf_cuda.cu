@@ -15,7 +15,9 @@
 
 #include "../../include/mrf_cuda.h"
 #include "common.cuh"
-#include "kernels_v1.cuh"
+#include "fwd_warp.cuh"
+#include "bwd_warp.cuh"
+#include "kernels_v1.cuh"  // aggregate + broadcast helpers
 #include "topology.hpp"
 
 using namespace mrf;
@@ -122,17 +124,24 @@ struct mrf_topology_s {
   std::vector<LineDesc> all_lines;                 // ISGMR: every direction, longest first
   std::vector<std::vector<LineDesc>> dir_lines;    // per direction, longest first
   std::vector<size_t> dir_start;                   // offset of dir r's block in the upload
+  std::vector<std::vector<LineDesc>> dir_lines_all;  // per direction incl. single-node lines (backward)
+  std::vector<size_t> dir_all_start;
   struct Dev {
-    LineDesc* lines = nullptr;  // [all_lines | dir 0 | dir 1 | ...]
+    LineDesc* lines = nullptr;  // [all_lines | dir 0 | ... | dir R-1 | all-lines dir 0 | ...]
   };
   std::map<int, Dev> dev;
   std::mutex mu;
 
   mrf_topology_s(int H, int W, int conn) : host(H, W, conn) {
     dir_lines.resize(host.num_dirs());
+    dir_lines_all.resize(host.num_dirs());
     for (int r = 0; r < host.num_dirs(); ++r) {
-      for (const Line& l : host.lines(r))
+      for (const Line& l : host.lines(r)) {
         if (l.length >= 2) dir_lines[r].push_back({l.first, l.length, l.edge_base, r});
+        dir_lines_all[r].push_back({l.first, l.length, l.edge_base, r});
+      }
+      std::stable_sort(dir_lines_all[r].begin(), dir_lines_all[r].end(),
+                       [](const LineDesc& a, const LineDesc& b) { return a.length > b.length; });
       std::stable_sort(dir_lines[r].begin(), dir_lines[r].end(),
                        [](const LineDesc& a, const LineDesc& b) { return a.length > b.length; });
       all_lines.insert(all_lines.end(), dir_lines[r].begin(), dir_lines[r].end());
@@ -143,6 +152,10 @@ struct mrf_topology_s {
     for (int r = 0; r < host.num_dirs(); ++r) {
       dir_start.push_back(off);
       off += dir_lines[r].size();
+    }
+    for (int r = 0; r < host.num_dirs(); ++r) {
+      dir_all_start.push_back(off);
+      off += dir_lines_all[r].size();
     }
   }
 
@@ -164,6 +177,7 @@ struct mrf_topology_s {
     if (it != dev.end()) return it->second.lines;
     std::vector<LineDesc> all(all_lines);
     for (auto& v : dir_lines) all.insert(all.end(), v.begin(), v.end());
+    for (auto& v : dir_lines_all) all.insert(all.end(), v.begin(), v.end());
     Dev dv;
     cuda_check(cudaMalloc(&dv.lines, sizeof(LineDesc) * std::max<size_t>(1, all.size())), "cudaMalloc(lines)");
     cuda_check(cudaMemcpy(dv.lines, all.data(), sizeof(LineDesc) * all.size(), cudaMemcpyHostToDevice),
@@ -215,33 +229,63 @@ size_t messages_bytes(mrf_topology_t topo, const mrf_problem_f32* pr) {
 
 int threads_for(int L) { return std::min(256, (L + 31) / 32 * 32); }
 
-struct FwdLaunch {
-  int table_mode;
-  size_t smem;
+// Per-call device description of V (banded vs dense strategy), stream-ordered.
+class PairDescHolder {
+ public:
+  PairDescHolder(const mrf_problem_f32* pr, int R, cudaStream_t s) : s_(s) {
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_), sizeof(PairDesc), s), "cudaMallocAsync(desc)");
+    const int64_t planes = int64_t(pr->batch) * (R / 2) * pr->height * pr->width;
+    ProfScope ps(s, MRF_KCLASS_AUX);
+    analyze_pairwise_kernel<<<1, 256, 0, s>>>(pr->pairwise, pr->labels, pr->weight_planes,
+                                              pr->weight_planes ? planes : 0, pr->weight, pr->rho_planes,
+                                              pr->rho_planes ? planes : 0, d_);
+    cuda_check(cudaGetLastError(), "analyze_pairwise launch");
+  }
+  ~PairDescHolder() { cudaFreeAsync(d_, s_); }
+  const PairDesc* get() const { return d_; }
+
+ private:
+  cudaStream_t s_;
+  PairDesc* d_ = nullptr;
 };
 
-FwdLaunch plan_forward(const mrf_problem_f32* pr) {
-  const int L = pr->labels;
-  const size_t head = sizeof(float) * (256 + 16);
-  const size_t tab = sizeof(float) * size_t(L) * L;
-  if (head + tab <= 200 * 1024) return {pr->weight_planes ? int(kTabV) : int(kTabWV), head + tab};
-  return {int(kTabGlobal), head};
+int epl_for(int L) {
+  if (L <= 32) return 1;
+  if (L <= 64) return 2;
+  if (L <= 128) return 4;
+  if (L <= 192) return 6;
+  return 8;
+}
+
+template <int EPL, bool TRWP>
+void launch_fwd_epl(const FwdArgs& a, int R, int batch, cudaStream_t stream) {
+  const int rows = 1 + (TRWP ? R - 1 : R - 2);
+  const int per_warp = fwd_warp_smem_floats(EPL, rows) * int(sizeof(float));
+  // few long chains (e.g. 375 rows of a KITTI frame) -> 1 warp per CTA so
+  // they spread over all SMs; many chains -> 4 warps per CTA
+  const int wpc = a.nlines >= 148 * 8 ? 4 : (a.nlines >= 148 * 2 ? 2 : 1);
+  const int smem = per_warp * wpc;
+  auto kern = fwd_warp_kernel<EPL, TRWP>;
+  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
+  const int blocks = std::min((a.nlines + wpc - 1) / wpc, 65535);
+  ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, stream>>>(a);
+  cuda_check(cudaGetLastError(), "fwd_warp_kernel launch");
 }
 
 template <bool TRWP>
-void launch_forward_sweep(mrf_topology_t topo, const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines,
-                          int nlines, const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k,
+void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines, int nlines,
+                          const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k, const PairDesc* desc,
                           cudaStream_t stream) {
   if (nlines == 0) return;
-  const FwdLaunch pl = plan_forward(pr);
-  auto kern = fwd_dense_kernel<TRWP>;
-  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem)),
-             "cudaFuncSetAttribute");
-  dim3 grid(std::min(nlines, 65535), pr->batch);
-  ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
-  kern<<<grid, threads_for(pr->labels), pl.smem, stream>>>(g, make_potentials(pr), lines, nlines, m_in, m_out, p, q,
-                                                           k, pl.table_mode);
-  cuda_check(cudaGetLastError(), "fwd_dense_kernel launch");
+  FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc};
+  switch (epl_for(pr->labels)) {
+    case 1: launch_fwd_epl<1, TRWP>(a, g.R, pr->batch, stream); break;
+    case 2: launch_fwd_epl<2, TRWP>(a, g.R, pr->batch, stream); break;
+    case 4: launch_fwd_epl<4, TRWP>(a, g.R, pr->batch, stream); break;
+    case 6: launch_fwd_epl<6, TRWP>(a, g.R, pr->batch, stream); break;
+    default: launch_fwd_epl<8, TRWP>(a, g.R, pr->batch, stream); break;
+  }
 }
 
 void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* messages, float* cost, uint16_t* labels,
@@ -257,25 +301,51 @@ void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* mess
 }
 
 void isgmr_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap, const float* m_in, float* m_out,
-                uint8_t* p, uint8_t* q, cudaStream_t stream) {
+                uint8_t* p, uint8_t* q, const PairDesc* desc, cudaStream_t stream) {
   const Geometry g = make_geometry(topo, pr, K_cap);
   const LineDesc* lines = topo->device_lines();
-  launch_forward_sweep<false>(topo, pr, g, lines, int(topo->all_lines.size()), m_in, m_out, p, q, k, stream);
+  launch_forward_sweep<false>(pr, g, lines, int(topo->all_lines.size()), m_in, m_out, p, q, k, desc, stream);
 }
 
 void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap, float* m, uint8_t* p, uint8_t* q,
-               cudaStream_t stream) {
+               const PairDesc* desc, cudaStream_t stream) {
   const Geometry g = make_geometry(topo, pr, K_cap);
   const LineDesc* lines = topo->device_lines();
   for (int r = 0; r < g.R; ++r)  // directions strictly sequential (trwp.hpp:50)
-    launch_forward_sweep<true>(topo, pr, g, lines + topo->dir_start[r], int(topo->dir_lines[r].size()), m, m, p, q,
-                               k, stream);
+    launch_forward_sweep<true>(pr, g, lines + topo->dir_start[r], int(topo->dir_lines[r].size()), m, m, p, q, k, desc,
+                               stream);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t vslot_bytes(mrf_topology_t topo, const mrf_problem_f32* pr) {
-  return sizeof(float) * size_t(pr->batch) * kBwdSlots * 2 * pr->labels * pr->labels;
+size_t gvacc_bytes(const mrf_problem_f32* pr) {
+  return sizeof(float) * size_t(pr->batch) * kVRep * 2 * pr->labels * pr->labels;
+}
+
+template <int EPL, bool TRWP>
+void launch_bwd_epl(const BwdArgs& a, int R, int batch, cudaStream_t stream) {
+  const int rowsF = 2 + (TRWP ? R - 1 : R - 2);
+  const int per_warp = bwd_warp_smem_floats(EPL, rowsF) * int(sizeof(float));
+  const int wpc = a.nlines >= 148 * 8 ? 4 : (a.nlines >= 148 * 2 ? 2 : 1);
+  const int smem = per_warp * wpc;
+  auto kern = bwd_warp_kernel<EPL, TRWP>;
+  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
+  const int blocks = std::min((a.nlines + wpc - 1) / wpc, 65535);
+  ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, stream>>>(a);
+  cuda_check(cudaGetLastError(), "bwd_warp_kernel launch");
+}
+
+template <bool TRWP>
+void launch_backward_sweep(const BwdArgs& a, int L, int R, int batch, cudaStream_t stream) {
+  if (a.nlines == 0) return;
+  switch (epl_for(L)) {
+    case 1: launch_bwd_epl<1, TRWP>(a, R, batch, stream); break;
+    case 2: launch_bwd_epl<2, TRWP>(a, R, batch, stream); break;
+    case 4: launch_bwd_epl<4, TRWP>(a, R, batch, stream); break;
+    case 6: launch_bwd_epl<6, TRWP>(a, R, batch, stream); break;
+    default: launch_bwd_epl<8, TRWP>(a, R, batch, stream); break;
+  }
 }
 
 template <bool TRWP>
@@ -283,13 +353,13 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
                   const float* grad_cost, const mrf_grads_f32* grads, void* ws, size_t ws_bytes,
                   cudaStream_t stream) {
   const int R = topo->host.num_dirs(), N = topo->host.nodes(), L = pr->labels, B = pr->batch;
-  const size_t mb = messages_bytes(topo, pr), vb = vslot_bytes(topo, pr);
+  const size_t mb = messages_bytes(topo, pr), vb = gvacc_bytes(pr);
   const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb);
   if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
   char* w = static_cast<char*>(ws);
   float* gm = reinterpret_cast<float*>(w);
   float* gnext = TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb));
-  float* vslots = reinterpret_cast<float*>(w + align_up(mb) * (TRWP ? 1 : 2));
+  float* gvacc = reinterpret_cast<float*>(w + align_up(mb) * (TRWP ? 1 : 2));
   const size_t NL = size_t(N) * L;
 
   // make_gradients (autodiff.hpp:33-44) and gm <- dc for every r (:72-74)
@@ -297,7 +367,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
              "copy grad_cost");
   if (grads->weight_planes)
     cuda_check(cudaMemsetAsync(grads->weight_planes, 0, sizeof(float) * B * (R / 2) * N, stream), "zero dw");
-  cuda_check(cudaMemsetAsync(vslots, 0, vb, stream), "zero dV slots");
+  cuda_check(cudaMemsetAsync(gvacc, 0, vb, stream), "zero dV accumulators");
   {
     const int64_t total = int64_t(B) * R * NL;
     ProfScope ps(stream, MRF_KCLASS_AUX);
@@ -309,34 +379,22 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   const Geometry g = make_geometry(topo, pr, K);
   const Potentials pot = make_potentials(pr);
   const LineDesc* lines = topo->device_lines();
-  const int nt = threads_for(L);
   for (int k = K - 1; k >= 0; --k) {
     for (int ri = 0; ri < R; ++ri) {
-      const int r = TRWP ? R - 1 - ri : ri;
-      const int nl = int(topo->dir_lines[r].size());
-      if (nl > 0) {
-        dim3 grid(std::min(nl, kBwdSlots), B);
-        // every image uses kBwdSlots slot columns; CTAs beyond nl never exist,
-        // their slots stay zero.
-        ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
-        bwd_dense_kernel<TRWP><<<grid, nt, 0, stream>>>(g, pot, lines + topo->dir_start[r], nl, r, p, q, k, gm, gnext,
-                                                        grads->unary, grads->weight_planes, vslots, kBwdSlots);
-        cuda_check(cudaGetLastError(), "bwd_dense_kernel launch");
-      }
-      if (TRWP)  // plane r consumed (autodiff.hpp:190-193)
-        cuda_check(cudaMemset2DAsync(gm + size_t(r) * NL, sizeof(float) * R * NL, 0, sizeof(float) * NL, B, stream),
-                   "zero plane");
+      const int r = TRWP ? R - 1 - ri : ri;  // TRWP replays directions in reverse (autodiff.hpp:147)
+      BwdArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), r, p, q, k,
+                gm, gnext, grads->unary, grads->weight_planes, gvacc};
+      // plane r of gm is consumed and left zero by the sweep (the reference's
+      // plane clear, autodiff.hpp:190-193, and swap-and-clear, :122-123)
+      launch_backward_sweep<TRWP>(a, L, R, B, stream);
     }
-    if (!TRWP) {  // swap and clear (autodiff.hpp:122-123)
-      std::swap(gm, gnext);
-      if (k > 0) cuda_check(cudaMemsetAsync(gnext, 0, mb, stream), "zero gm_next");
-    }
+    if (!TRWP) std::swap(gm, gnext);
   }
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
     ProfScope ps(stream, MRF_KCLASS_AUX);
-    reduce_vslots_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, kBwdSlots, L, vslots, grads->pairwise);
-    cuda_check(cudaGetLastError(), "reduce_vslots launch");
+    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, gvacc, grads->pairwise);
+    cuda_check(cudaGetLastError(), "reduce_gvacc launch");
   }
 }
 
@@ -412,10 +470,11 @@ int mrf_isgmr_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
     cuda_check(cudaMemsetAsync(bufs[1], 0, mb, stream), "zero mhat");
     // Iteration k writes bufs[(K-1-k)&1] so the last one lands in out->messages;
     // the publish m <- mhat (isgmr.hpp:55) is the buffer swap.
+    PairDescHolder desc(prob, topo->host.num_dirs(), stream);
     for (int k = 0; k < iterations; ++k) {
       float* dst = bufs[(iterations - 1 - k) & 1];
       const float* src = bufs[(iterations - k) & 1];
-      isgmr_step(topo, prob, k, iterations, src, dst, out->p, out->q, stream);
+      isgmr_step(topo, prob, k, iterations, src, dst, out->p, out->q, desc.get(), stream);
     }
     launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
   });
@@ -431,7 +490,9 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
     if (iterations < 1) fail(MRF_EINVAL, "trwp_forward: iterations must be >= 1");
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
     cuda_check(cudaMemsetAsync(out->messages, 0, messages_bytes(topo, prob), stream), "zero m");
-    for (int k = 0; k < iterations; ++k) trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, stream);
+    PairDescHolder desc(prob, topo->host.num_dirs(), stream);
+    for (int k = 0; k < iterations; ++k)
+      trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, desc.get(), stream);
     launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
   });
 }
@@ -442,7 +503,8 @@ int mrf_isgmr_step_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int k, 
     validate_problem(topo, prob);
     if (k < 0 || k >= K_cap) fail(MRF_EINVAL, "iteration index out of range");
     if (!m_in || !m_out || !p || !q || m_in == m_out) fail(MRF_EINVAL, "bad step buffers");
-    isgmr_step(topo, prob, k, K_cap, m_in, m_out, p, q, stream);
+    PairDescHolder desc(prob, topo->host.num_dirs(), stream);
+    isgmr_step(topo, prob, k, K_cap, m_in, m_out, p, q, desc.get(), stream);
   });
 }
 
@@ -453,7 +515,8 @@ int mrf_trwp_step_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int k, i
     validate_rho(prob);
     if (k < 0 || k >= K_cap) fail(MRF_EINVAL, "iteration index out of range");
     if (!messages || !p || !q) fail(MRF_EINVAL, "bad step buffers");
-    trwp_step(topo, prob, k, K_cap, messages, p, q, stream);
+    PairDescHolder desc(prob, topo->host.num_dirs(), stream);
+    trwp_step(topo, prob, k, K_cap, messages, p, q, desc.get(), stream);
   });
 }
 
@@ -470,7 +533,7 @@ size_t mrf_backward_workspace_bytes(mrf_topology_t topo, const mrf_problem_f32* 
   (void)iterations;
   if (!topo || !prob) return 0;
   const size_t mb = align_up(messages_bytes(topo, prob));
-  return mb * (engine == MRF_ENGINE_ISGMR ? 2 : 1) + align_up(vslot_bytes(topo, prob));
+  return mb * (engine == MRF_ENGINE_ISGMR ? 2 : 1) + align_up(gvacc_bytes(prob));
 }
 
 int mrf_isgmr_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const uint8_t* p,
