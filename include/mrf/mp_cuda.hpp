@@ -1,0 +1,575 @@
+// mrf/mp_cuda.hpp -- C++ drop-in for the reference library's hot path.
+//
+// A user of the reference (/root/reference/proj, namespace mp) who includes
+// <mp/isgmr.hpp>, <mp/trwp.hpp>, <mp/autodiff.hpp> and calls
+//   mp::isgmr_forward<float>(topo, pots, K, threads)        isgmr.hpp:145-152
+//   mp::trwp_forward<float>(topo, pots, rho, K, threads)    trwp.hpp:148-156
+//   mp::isgmr_backward<float>(topo, pots, indices, dc, t)   autodiff.hpp:63-126
+//   mp::trwp_backward<float>(topo, pots, rho, indices, dc, t) autodiff.hpp:133-197
+// includes this header instead and links libmrf_cuda.so. Types, names,
+// layouts and exceptions follow the reference (grid.hpp, potentials.hpp,
+// index_store.hpp, inference.hpp, autodiff.hpp); `threads` is accepted and
+// ignored; every computation runs on the current CUDA device through the
+// C-ABI (include/mrf_cuda.h), with host<->device copies of the std::vector
+// arguments and results. Only Real = float exists here: the double
+// instantiation of the reference stays a CPU tool (gradient checking).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include <cuda_runtime_api.h>
+
+#include "../mrf_cuda.h"
+
+namespace mp {
+
+inline constexpr int kMaxLabels = 256;
+
+namespace cuda_detail {
+
+inline void check(int rc) {
+  if (rc == MRF_OK) return;
+  if (rc == MRF_EINVAL) throw std::invalid_argument(mrf_last_error());
+  throw std::runtime_error(std::string("mrf_cuda: ") + mrf_last_error());
+}
+inline void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owning device allocation (stream-ordered on the legacy default stream).
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t bytes) : bytes_(bytes) {
+    if (bytes) check_cuda(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(std::exchange(o.ptr_, nullptr)), bytes_(o.bytes_) {}
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      if (ptr_) cudaFree(ptr_);
+      ptr_ = std::exchange(o.ptr_, nullptr);
+      bytes_ = o.bytes_;
+    }
+    return *this;
+  }
+  ~DeviceBuffer() {
+    if (ptr_) cudaFree(ptr_);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr_);
+  }
+  size_t bytes() const { return bytes_; }
+
+  template <class T>
+  static DeviceBuffer upload(const T* src, size_t count) {
+    DeviceBuffer b(sizeof(T) * count);
+    if (count) check_cuda(cudaMemcpy(b.ptr_, src, sizeof(T) * count, cudaMemcpyHostToDevice), "H2D");
+    return b;
+  }
+  template <class T>
+  void download(T* dst, size_t count) const {
+    if (count) check_cuda(cudaMemcpy(dst, ptr_, sizeof(T) * count, cudaMemcpyDeviceToHost), "D2H");
+  }
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+}  // namespace cuda_detail
+
+// ------------------------------------------------------------------ geometry
+
+/// grid.hpp:11-25
+struct GridGraph {
+  int height = 0;
+  int width = 0;
+  GridGraph() = default;
+  GridGraph(int h, int w) : height(h), width(w) {
+    if (h < 1 || w < 1) throw std::invalid_argument("GridGraph: H and W must be >= 1");
+  }
+  int nodes() const { return height * width; }
+  int id(int h, int w) const { return h * width + w; }
+  std::pair<int, int> coords(int node) const { return {node / width, node % width}; }
+  bool contains(int h, int w) const { return h >= 0 && h < height && w >= 0 && w < width; }
+};
+
+/// grid.hpp:29-33
+struct Direction {
+  int dh = 0;
+  int dw = 0;
+  int opposite = -1;
+};
+
+/// grid.hpp:38-50; order E,W,S,N,SE,NW,SW,NE,... with opposite = r^1.
+class DirectionSet {
+ public:
+  static DirectionSet build(int connectivity) {
+    if (connectivity != 4 && connectivity != 8 && connectivity != 16)
+      throw std::invalid_argument("DirectionSet: connectivity must be 4, 8 or 16");
+    static const int k[16][2] = {{0, 1},  {0, -1},  {1, 0},  {-1, 0}, {1, 1},  {-1, -1}, {1, -1}, {-1, 1},
+                                 {1, 2},  {-1, -2}, {1, -2}, {-1, 2}, {2, 1},  {-2, -1}, {2, -1}, {-2, 1}};
+    DirectionSet s;
+    for (int r = 0; r < connectivity; ++r) s.dirs_.push_back(Direction{k[r][0], k[r][1], r ^ 1});
+    return s;
+  }
+  int size() const { return static_cast<int>(dirs_.size()); }
+  int connectivity() const { return size(); }
+  int families() const { return size() / 2; }
+  const Direction& operator[](int r) const { return dirs_[r]; }
+  const std::vector<Direction>& all() const { return dirs_; }
+
+ private:
+  std::vector<Direction> dirs_;
+};
+
+/// grid.hpp:53-57
+struct Scanline {
+  int direction = -1;
+  std::pair<int, int> first_node{};
+  std::vector<int32_t> nodes;
+};
+
+/// grid.hpp:73-96. Geometry is computed by libmrf_cuda (identical scanline
+/// order and edge numbering); the handle also carries the device line tables.
+class GridTopology {
+ public:
+  GridTopology(const GridGraph& g, DirectionSet dirs) : grid_(g), dirs_(std::move(dirs)) {
+    mrf_topology_t h = nullptr;
+    cuda_detail::check(mrf_topology_create(g.height, g.width, dirs_.size(), &h));
+    handle_ = std::shared_ptr<mrf_topology_s>(h, [](mrf_topology_t t) { mrf_topology_destroy(t); });
+    const int R = dirs_.size();
+    edge_count_.resize(R);
+    dir_offset_.resize(R);
+    int nd = 0;
+    cuda_detail::check(mrf_topology_info(h, &nd, &total_edges_, edge_count_.data(), dir_offset_.data()));
+    edge_index_.assign(size_t(R) * g.nodes(), -1);
+    cuda_detail::check(mrf_topology_edge_index(h, edge_index_.data()));
+    scanlines_.resize(R);
+    for (int r = 0; r < R; ++r) {
+      int32_t cnt = 0;
+      cuda_detail::check(mrf_topology_scanlines(h, r, nullptr, nullptr, &cnt, 0));
+      std::vector<int32_t> first(cnt), len(cnt);
+      cuda_detail::check(mrf_topology_scanlines(h, r, first.data(), len.data(), &cnt, cnt));
+      const int step = dirs_[r].dh * g.width + dirs_[r].dw;
+      for (int t = 0; t < cnt; ++t) {
+        Scanline sl;
+        sl.direction = r;
+        for (int j = 0; j < len[t]; ++j) sl.nodes.push_back(first[t] + j * step);
+        sl.first_node = g.coords(sl.nodes.front());
+        scanlines_[r].push_back(std::move(sl));
+      }
+    }
+  }
+
+  const GridGraph& grid() const { return grid_; }
+  const DirectionSet& dirs() const { return dirs_; }
+  int num_dirs() const { return dirs_.size(); }
+  const std::vector<Scanline>& scanlines(int r) const { return scanlines_[r]; }
+  int32_t edge_index(int r, int node) const { return edge_index_[size_t(r) * grid_.nodes() + node]; }
+  std::int64_t edge_count(int r) const { return edge_count_[r]; }
+  std::int64_t total_edges() const { return total_edges_; }
+  std::int64_t dir_offset(int r) const { return dir_offset_[r]; }
+  mrf_topology_t handle() const { return handle_.get(); }
+
+ private:
+  GridGraph grid_;
+  DirectionSet dirs_;
+  std::shared_ptr<mrf_topology_s> handle_;
+  std::vector<std::vector<Scanline>> scanlines_;
+  std::vector<int32_t> edge_index_;
+  std::vector<std::int64_t> edge_count_, dir_offset_;
+  std::int64_t total_edges_ = 0;
+};
+
+// --------------------------------------------------------------- potentials
+
+enum class PairwiseKind { potts, truncated_linear, truncated_quadratic, sgm_p1p2, explicit_matrix };
+
+struct PairwiseParams {
+  double trunc = -1.0;
+  double p1 = 1.0;
+  double p2 = 1.0;
+};
+
+/// potentials.hpp:27-35
+template <class Real>
+struct PairwiseFunction {
+  PairwiseKind kind = PairwiseKind::potts;
+  int labels = 0;
+  std::vector<Real> table;
+  Real operator()(int a, int b) const { return table[a * labels + b]; }
+  Real& at(int a, int b) { return table[a * labels + b]; }
+};
+
+/// potentials.hpp:38-72: built-ins computed in double from |a-b|, cast.
+template <class Real>
+PairwiseFunction<Real> build_pairwise(PairwiseKind kind, const PairwiseParams& params, int labels) {
+  if (labels < 1 || labels > kMaxLabels) throw std::invalid_argument("build_pairwise: label count must be in [1, 256]");
+  PairwiseFunction<Real> v;
+  v.kind = kind;
+  v.labels = labels;
+  v.table.assign(size_t(labels) * labels, Real(0));
+  for (int a = 0; a < labels; ++a)
+    for (int b = 0; b < labels; ++b) {
+      const double d = std::abs(a - b);
+      double val = 0.0;
+      switch (kind) {
+        case PairwiseKind::potts: val = a == b ? 0.0 : 1.0; break;
+        case PairwiseKind::truncated_linear:
+          if (params.trunc <= 0) throw std::invalid_argument("truncated_linear: trunc must be > 0");
+          val = d < params.trunc ? d : params.trunc;
+          break;
+        case PairwiseKind::truncated_quadratic:
+          if (params.trunc <= 0) throw std::invalid_argument("truncated_quadratic: trunc must be > 0");
+          val = d * d < params.trunc ? d * d : params.trunc;
+          break;
+        case PairwiseKind::sgm_p1p2:
+          if (!(0 < params.p1 && params.p1 <= params.p2)) throw std::invalid_argument("sgm_p1p2: need 0 < P1 <= P2");
+          val = a == b ? 0.0 : (d == 1.0 ? params.p1 : params.p2);
+          break;
+        case PairwiseKind::explicit_matrix:
+          throw std::invalid_argument("build_pairwise: explicit_matrix takes a user table");
+      }
+      v.at(a, b) = static_cast<Real>(val);
+    }
+  return v;
+}
+
+template <class Real>
+PairwiseFunction<Real> explicit_pairwise(std::vector<Real> table, int labels) {
+  if (table.size() != size_t(labels) * labels) throw std::invalid_argument("explicit_pairwise: table size mismatch");
+  PairwiseFunction<Real> v;
+  v.kind = PairwiseKind::explicit_matrix;
+  v.labels = labels;
+  v.table = std::move(table);
+  return v;
+}
+
+/// potentials.hpp:88-105
+template <class Real>
+struct UnaryVolume {
+  int height = 0, width = 0, labels = 0;
+  std::vector<Real> values;
+  UnaryVolume() = default;
+  UnaryVolume(int h, int w, int l, Real fill = Real(0)) : height(h), width(w), labels(l), values(size_t(h) * w * l, fill) {
+    if (l < 1 || l > kMaxLabels) throw std::invalid_argument("UnaryVolume: label count must be in [1, 256]");
+  }
+  Real at(int node, int label) const { return values[size_t(node) * labels + label]; }
+  Real& at(int node, int label) { return values[size_t(node) * labels + label]; }
+  const Real* row(int node) const { return values.data() + size_t(node) * labels; }
+  int nodes() const { return height * width; }
+};
+
+/// potentials.hpp:113-139
+template <class Real>
+class EdgeWeights {
+ public:
+  static EdgeWeights constant(Real w) {
+    if (!(w >= 0)) throw std::invalid_argument("EdgeWeights: weights must be nonnegative");
+    EdgeWeights e;
+    e.constant_ = w;
+    return e;
+  }
+  static EdgeWeights planes(std::vector<std::vector<Real>> planes) {
+    EdgeWeights e;
+    e.planes_ = std::move(planes);
+    return e;
+  }
+  bool is_constant() const { return planes_.empty(); }
+  const std::vector<std::vector<Real>>& plane_data() const { return planes_; }
+  std::vector<std::vector<Real>>& plane_data() { return planes_; }
+  Real weight(int r, int prev, int cur) const {
+    if (planes_.empty()) return constant_;
+    return planes_[r >> 1][(r & 1) ? cur : prev];
+  }
+  static int plane_node(int r, int prev, int cur) { return (r & 1) ? cur : prev; }
+
+ private:
+  Real constant_ = Real(1);
+  std::vector<std::vector<Real>> planes_;
+};
+
+/// potentials.hpp:143-163
+template <class Real>
+struct TreeCoefficients {
+  Real uniform = Real(0.5);
+  std::vector<std::vector<Real>> planes;
+  Real at(int r, int prev, int cur) const {
+    if (planes.empty()) return uniform;
+    return planes[r >> 1][(r & 1) ? cur : prev];
+  }
+};
+
+template <class Real>
+TreeCoefficients<Real> default_rho(int connectivity, Real value = Real(0.5)) {
+  DirectionSet::build(connectivity);
+  if (!(value > 0 && value <= 1)) throw std::invalid_argument("rho must be in (0, 1]");
+  return TreeCoefficients<Real>{value, {}};
+}
+
+template <class Real>
+struct PotentialSet {
+  UnaryVolume<Real> unary;
+  PairwiseFunction<Real> pairwise;
+  EdgeWeights<Real> weights = EdgeWeights<Real>::constant(Real(1));
+};
+
+// --------------------------------------------------------------- outputs
+
+/// index_store.hpp:16-58 (same byte layout; filled from the device)
+class IndexStore {
+ public:
+  IndexStore(const GridTopology& topo, int labels) : labels_(labels), edges_(topo.total_edges()) {}
+  void append_iteration() {
+    ++iterations_;
+    p_.resize(size_t(iterations_) * edges_ * labels_, 0);
+    q_.resize(size_t(iterations_) * edges_, 0);
+  }
+  int iterations() const { return iterations_; }
+  const std::vector<std::uint8_t>& p_data() const { return p_; }
+  const std::vector<std::uint8_t>& q_data() const { return q_; }
+  std::vector<std::uint8_t>& p_data() { return p_; }
+  std::vector<std::uint8_t>& q_data() { return q_; }
+  int labels() const { return labels_; }
+  std::int64_t edges() const { return edges_; }
+  size_t bytes() const { return p_.size() + q_.size(); }
+  std::uint8_t* p_row(const GridTopology& topo, int k, int r, int32_t e) { return p_.data() + flat(topo, k, r, e) * labels_; }
+  const std::uint8_t* p_row(const GridTopology& topo, int k, int r, int32_t e) const {
+    return p_.data() + flat(topo, k, r, e) * labels_;
+  }
+  std::uint8_t& q_at(const GridTopology& topo, int k, int r, int32_t e) { return q_[flat(topo, k, r, e)]; }
+  std::uint8_t q_at(const GridTopology& topo, int k, int r, int32_t e) const { return q_[flat(topo, k, r, e)]; }
+
+ private:
+  size_t flat(const GridTopology& topo, int k, int r, int32_t e) const {
+    return size_t(k) * edges_ + topo.dir_offset(r) + e;
+  }
+  int labels_ = 0;
+  int iterations_ = 0;
+  std::int64_t edges_ = 0;
+  std::vector<std::uint8_t> p_, q_;
+};
+
+/// inference.hpp:16-23
+template <class Real>
+struct CostOutput {
+  int height = 0, width = 0, labels = 0;
+  std::vector<Real> cost;
+  std::vector<std::uint16_t> labels_map;
+  const Real* row(int node) const { return cost.data() + size_t(node) * labels; }
+};
+
+/// inference.hpp:62-68. min_argmin_gap is a diagnostic the GPU path does not
+/// track; it is +inf.
+template <class Real>
+struct ForwardResult {
+  CostOutput<Real> output;
+  std::vector<Real> messages;
+  IndexStore indices;
+  Real min_argmin_gap;
+};
+
+/// autodiff.hpp:17-29
+template <class Real>
+struct GradientSet {
+  std::vector<Real> unary;
+  std::vector<Real> pairwise;
+  std::vector<std::vector<Real>> edge_weights;
+  Real edge_weight_total() const {
+    Real s = Real(0);
+    for (const auto& p : edge_weights)
+      for (Real v : p) s += v;
+    return s;
+  }
+};
+
+// ------------------------------------------------------------ entry points
+
+namespace cuda_detail {
+
+template <class Real>
+constexpr void require_float() {
+  static_assert(std::is_same_v<Real, float>, "mrf_cuda computes in FP32; use the CPU reference for Real=double");
+}
+
+struct DeviceProblem {
+  DeviceBuffer unary, V, wplanes, rplanes;
+  mrf_problem_f32 prob{};
+};
+
+inline std::vector<float> flatten(const std::vector<std::vector<float>>& planes, size_t n, int fam) {
+  std::vector<float> out(size_t(fam) * n);
+  if (planes.size() != size_t(fam)) throw std::invalid_argument("plane count mismatch");
+  for (int f = 0; f < fam; ++f) {
+    if (planes[f].size() != n) throw std::invalid_argument("plane size mismatch");
+    std::memcpy(out.data() + f * n, planes[f].data(), sizeof(float) * n);
+  }
+  return out;
+}
+
+inline DeviceProblem upload(const GridTopology& topo, const PotentialSet<float>& pots, const TreeCoefficients<float>* rho,
+                            bool check_finite) {
+  const auto& u = pots.unary;
+  const int L = u.labels;
+  if (L > kMaxLabels) throw std::invalid_argument("engine: more than 256 labels");
+  if (u.height != topo.grid().height || u.width != topo.grid().width)
+    throw std::invalid_argument("unary volume does not match the topology");
+  if (check_finite)
+    for (float v : u.values)
+      if (!std::isfinite(static_cast<double>(v))) throw std::invalid_argument("engine: non-finite unary potential");
+  if (pots.pairwise.labels != L || pots.pairwise.table.size() != size_t(L) * L)
+    throw std::invalid_argument("pairwise table does not match the label count");
+  DeviceProblem d;
+  const size_t n = size_t(topo.grid().nodes());
+  const int fam = topo.num_dirs() / 2;
+  d.unary = DeviceBuffer::upload(u.values.data(), u.values.size());
+  d.V = DeviceBuffer::upload(pots.pairwise.table.data(), pots.pairwise.table.size());
+  d.prob.batch = 1;
+  d.prob.height = u.height;
+  d.prob.width = u.width;
+  d.prob.labels = L;
+  d.prob.unary = d.unary.as<float>();
+  d.prob.pairwise = d.V.as<float>();
+  if (pots.weights.is_constant()) {
+    d.prob.weight = pots.weights.weight(0, 0, 0);
+  } else {
+    const auto flat = flatten(pots.weights.plane_data(), n, fam);
+    d.wplanes = DeviceBuffer::upload(flat.data(), flat.size());
+    d.prob.weight_planes = d.wplanes.as<float>();
+  }
+  d.prob.rho = 0.5f;
+  if (rho) {
+    if (rho->planes.empty()) {
+      d.prob.rho = rho->uniform;
+    } else {
+      const auto flat = flatten(rho->planes, n, fam);
+      d.rplanes = DeviceBuffer::upload(flat.data(), flat.size());
+      d.prob.rho_planes = d.rplanes.as<float>();
+    }
+  }
+  return d;
+}
+
+inline ForwardResult<float> forward(int engine, const GridTopology& topo, const PotentialSet<float>& pots,
+                                    const TreeCoefficients<float>* rho, int K) {
+  if (K < 1)
+    throw std::invalid_argument(engine == MRF_ENGINE_ISGMR ? "isgmr_forward: iterations must be >= 1"
+                                                           : "trwp_forward: iterations must be >= 1");
+  DeviceProblem d = upload(topo, pots, rho, true);
+  const int L = d.prob.labels, R = topo.num_dirs();
+  const size_t n = size_t(topo.grid().nodes()), E = size_t(topo.total_edges());
+  DeviceBuffer cost(sizeof(float) * n * L), labels(2 * n), msg(sizeof(float) * R * n * L), p(size_t(K) * E * L + 4),
+      q(size_t(K) * E + 4);
+  const size_t wsb = mrf_forward_workspace_bytes(topo.handle(), &d.prob, engine, K);
+  DeviceBuffer ws(wsb);
+  mrf_forward_out out{cost.as<float>(), labels.as<uint16_t>(), msg.as<float>(), p.as<uint8_t>(), q.as<uint8_t>()};
+  if (engine == MRF_ENGINE_ISGMR)
+    check(mrf_isgmr_forward_f32(topo.handle(), &d.prob, K, &out, ws.as<void>(), wsb, nullptr));
+  else
+    check(mrf_trwp_forward_f32(topo.handle(), &d.prob, K, &out, ws.as<void>(), wsb, nullptr));
+  ForwardResult<float> res{CostOutput<float>{}, {}, IndexStore(topo, L), std::numeric_limits<float>::infinity()};
+  res.output.height = topo.grid().height;
+  res.output.width = topo.grid().width;
+  res.output.labels = L;
+  res.output.cost.resize(n * L);
+  res.output.labels_map.resize(n);
+  res.messages.resize(size_t(R) * n * L);
+  for (int k = 0; k < K; ++k) res.indices.append_iteration();
+  cost.download(res.output.cost.data(), n * L);
+  labels.download(res.output.labels_map.data(), n);
+  msg.download(res.messages.data(), res.messages.size());
+  p.download(res.indices.p_data().data(), res.indices.p_data().size());
+  q.download(res.indices.q_data().data(), res.indices.q_data().size());
+  return res;
+}
+
+inline GradientSet<float> backward(int engine, const GridTopology& topo, const PotentialSet<float>& pots,
+                                   const TreeCoefficients<float>* rho, const IndexStore& indices,
+                                   const std::vector<float>& grad_cost) {
+  const size_t n = size_t(topo.grid().nodes());
+  const int L = pots.unary.labels, R = topo.num_dirs();
+  if (grad_cost.size() != n * L) throw std::invalid_argument("backward: cost gradient size mismatch");
+  if (indices.labels() != L || indices.edges() != topo.total_edges())
+    throw std::invalid_argument("backward: index store does not match the problem");
+  const int K = indices.iterations();
+  DeviceProblem d = upload(topo, pots, rho, false);
+  DeviceBuffer p = DeviceBuffer::upload(indices.p_data().data(), indices.p_data().size() + 4);
+  DeviceBuffer q = DeviceBuffer::upload(indices.q_data().data(), indices.q_data().size() + 4);
+  DeviceBuffer gc = DeviceBuffer::upload(grad_cost.data(), grad_cost.size());
+  DeviceBuffer gu(sizeof(float) * n * L), gv(sizeof(float) * L * L), gw(sizeof(float) * (R / 2) * n);
+  const size_t wsb = mrf_backward_workspace_bytes(topo.handle(), &d.prob, engine, K);
+  DeviceBuffer ws(wsb);
+  mrf_grads_f32 g{gu.as<float>(), gv.as<float>(), gw.as<float>()};
+  if (engine == MRF_ENGINE_ISGMR)
+    check(mrf_isgmr_backward_f32(topo.handle(), &d.prob, K, p.as<uint8_t>(), q.as<uint8_t>(), gc.as<float>(), &g,
+                                 ws.as<void>(), wsb, nullptr));
+  else
+    check(mrf_trwp_backward_f32(topo.handle(), &d.prob, K, p.as<uint8_t>(), q.as<uint8_t>(), gc.as<float>(), &g,
+                                ws.as<void>(), wsb, nullptr));
+  GradientSet<float> out;
+  out.unary.resize(n * L);
+  out.pairwise.resize(size_t(L) * L);
+  out.edge_weights.assign(R / 2, std::vector<float>(n));
+  gu.download(out.unary.data(), out.unary.size());
+  gv.download(out.pairwise.data(), out.pairwise.size());
+  std::vector<float> flat((R / 2) * n);
+  gw.download(flat.data(), flat.size());
+  for (int f = 0; f < R / 2; ++f) std::memcpy(out.edge_weights[f].data(), flat.data() + f * n, sizeof(float) * n);
+  return out;
+}
+
+}  // namespace cuda_detail
+
+/// isgmr.hpp:145-152
+template <class Real>
+ForwardResult<Real> isgmr_forward(const GridTopology& topo, const PotentialSet<Real>& pots, int iterations,
+                                  int threads = 1) {
+  cuda_detail::require_float<Real>();
+  (void)threads;
+  return cuda_detail::forward(MRF_ENGINE_ISGMR, topo, pots, nullptr, iterations);
+}
+
+/// trwp.hpp:148-156
+template <class Real>
+ForwardResult<Real> trwp_forward(const GridTopology& topo, const PotentialSet<Real>& pots,
+                                 const TreeCoefficients<Real>& rho, int iterations, int threads = 1) {
+  cuda_detail::require_float<Real>();
+  (void)threads;
+  if (rho.planes.empty() && !(rho.uniform > 0 && rho.uniform <= 1)) throw std::invalid_argument("rho must be in (0, 1]");
+  return cuda_detail::forward(MRF_ENGINE_TRWP, topo, pots, &rho, iterations);
+}
+
+/// autodiff.hpp:63-126
+template <class Real>
+GradientSet<Real> isgmr_backward(const GridTopology& topo, const PotentialSet<Real>& pots, const IndexStore& indices,
+                                 const std::vector<Real>& grad_cost, int threads = 1) {
+  cuda_detail::require_float<Real>();
+  (void)threads;
+  return cuda_detail::backward(MRF_ENGINE_ISGMR, topo, pots, nullptr, indices, grad_cost);
+}
+
+/// autodiff.hpp:133-197
+template <class Real>
+GradientSet<Real> trwp_backward(const GridTopology& topo, const PotentialSet<Real>& pots,
+                                const TreeCoefficients<Real>& rho, const IndexStore& indices,
+                                const std::vector<Real>& grad_cost, int threads = 1) {
+  cuda_detail::require_float<Real>();
+  (void)threads;
+  return cuda_detail::backward(MRF_ENGINE_TRWP, topo, pots, &rho, indices, grad_cost);
+}
+
+}  // namespace mp

@@ -161,7 +161,9 @@ def test_backward_deterministic_run_to_run():
         b = gpu_backward(engine, mrf, f, gc)
         assert torch.equal(a.unary, b.unary)
         assert torch.equal(a.edge_weights, b.edge_weights)
-        assert torch.allclose(a.pairwise, b.pairwise, rtol=1e-6, atol=1e-7)
+        from tests.gpu_util import normwise
+
+        assert normwise(a.pairwise.cpu().numpy(), b.pairwise.cpu().numpy()) <= 1e-6
 
 
 def test_invalid_arguments_raise():
