@@ -1,55 +1,81 @@
-"""In-tree build of libmrf_cuda.so for sm_100a (nvcc cross-compiles; no GPU needed)."""
+"""In-tree build of libmrf_cuda.so for sm_100a (nvcc cross-compiles; no GPU needed).
+
+Translation units are compiled in parallel to objects under build/, then
+linked into paper_1910_10892_b200/libmrf_cuda.so.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = [os.path.join(HERE, "csrc", f) for f in ("mrf_cuda.cu", "misc.cu", "topology.cpp")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))
-              if f.endswith((".cuh", ".hpp"))] + [os.path.join(ROOT, "include", "mrf_cuda.h")]
+CSRC = os.path.join(HERE, "csrc")
+UNITS = ["mrf_cuda.cu", "misc.cu", "topology.cpp", "fwd_generic.cu", "fwd_band2_isgmr.cu", "fwd_band2_trwp.cu",
+         "bwd.cu"]
 OUT = os.path.join(HERE, "libmrf_cuda.so")
+OBJDIR = os.path.join(ROOT, "build", "mrf_cuda")
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ARCH + [
     "-lineinfo", "-O3", "-std=c++17",
     # Bit-exact argmins need one rounding per operation: no FMA contraction,
     # IEEE division/sqrt, no flush-to-zero (SURVEY.md §7 hard part 1).
     "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
-    "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "-Xcompiler", "-fPIC", "-Xptxas", "-v",
 ]
 
 
 def nvcc() -> str:
-    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
-        if c and (os.path.isabs(c) and os.path.exists(c) or not os.path.isabs(c)):
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc"):
+        if c and os.path.exists(c):
             return c
     return "nvcc"
+
+
+def _deps():
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh", ".hpp", ".cpp"))]
+    return deps + [os.path.join(ROOT, "include", "mrf_cuda.h"), __file__]
 
 
 def up_to_date() -> bool:
     if not os.path.exists(OUT):
         return False
     t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(d) <= t for d in DEPS if os.path.exists(d))
+    return all(os.path.getmtime(d) <= t for d in _deps())
+
+
+def _compile(unit: str):
+    src = os.path.join(CSRC, unit)
+    obj = os.path.join(OBJDIR, unit + ".o")
+    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    return obj, res.stderr
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", OUT + ".tmp", *SRC]
+    os.makedirs(OBJDIR, exist_ok=True)
+    workers = max(1, min(len(UNITS), os.cpu_count() or 1))
+    with cf.ThreadPoolExecutor(workers) as ex:
+        results = list(ex.map(_compile, UNITS))
+    objs = [o for o, _ in results]
+    cmd = [nvcc(), *ARCH, "-shared", "-o", OUT + ".tmp", *objs]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+        raise RuntimeError("link failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
     os.replace(OUT + ".tmp", OUT)
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(res.stderr)
+        f.write("".join(log for _, log in results))
     if verbose:
-        print(res.stderr, file=sys.stderr)
+        print("".join(log for _, log in results), file=sys.stderr)
     return OUT
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

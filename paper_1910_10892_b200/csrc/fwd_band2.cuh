@@ -1,0 +1,288 @@
+// Forward sweep specialised for banded pairwise terms with D == 2 (V(a,b) =
+// g(|a-b|), g(d) = g(2) for d >= 2: truncated linear tau <= 2, Potts-like
+// P1/P2, ... -- the stereo configurations C1-C3) and 4 / 8 directions.
+//
+// Same exact algorithm as the banded path of fwd_warp.cuh (see there), with
+// everything the per-node chain touches kept in registers and shuffles:
+// compile-time R unrolls the plane loops, FULL (L == 32*EPL) drops all
+// per-label validity handling, invalid labels are carried as +inf instead of
+// branches, and p bytes are packed into one store per lane.
+#pragma once
+
+#include "fwd_warp.cuh"
+
+namespace mrf {
+
+__host__ __device__ constexpr int band2_smem_floats(int EPL, int rows) {
+  return ((kStages * rows) * 32 * EPL + kStages * 64 + 31) / 32 * 32;
+}
+
+// EPL bytes (one per label) -> one (or a few) packed stores at row + l0.
+template <int EPL, bool FULL>
+__device__ __forceinline__ void store_p(uint8_t* row, int l0, const int (&am)[EPL], int nvalid) {
+  if (FULL && EPL % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < EPL; i += 4) {
+      const uint32_t w = uint32_t(am[i]) | (uint32_t(am[i + 1]) << 8) | (uint32_t(am[i + 2]) << 16) |
+                         (uint32_t(am[i + 3]) << 24);
+      *reinterpret_cast<uint32_t*>(row + l0 + i) = w;
+    }
+  } else if (FULL && EPL % 2 == 0) {
+#pragma unroll
+    for (int i = 0; i < EPL; i += 2)
+      *reinterpret_cast<uint16_t*>(row + l0 + i) = uint16_t(am[i] | (am[i + 1] << 8));
+  } else {
+#pragma unroll
+    for (int i = 0; i < EPL; ++i)
+      if (FULL || i < nvalid) row[l0 + i] = uint8_t(am[i]);
+  }
+}
+
+template <int EPL, bool TRWP, int R, bool FULL>
+__global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
+  if (!(a.desc->banded && a.desc->D == 2)) return;  // fwd_warp_kernel handles it
+  extern __shared__ float smem[];
+  constexpr int NP = TRWP ? R - 1 : R - 2;
+  constexpr int ROWS = NP + 1;
+  constexpr int LS = 32 * EPL;
+  const Geometry& g = a.g;
+  const int L = g.L, N = g.N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  float* ring = smem + size_t(wid) * band2_smem_floats(EPL, ROWS);
+  float* s_x = ring + kStages * ROWS * LS;
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const uint32_t x_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_x));
+
+  const int b = blockIdx.y;
+  const float* un = a.pot.unary + size_t(b) * N * L;
+  const size_t img = size_t(b) * R * N * L;
+  const int l0 = lane * EPL;
+  const int nvalid = FULL ? EPL : min(EPL, max(0, L - l0));
+  const int chunk = (FULL || nvalid == EPL) ? Chunk<EPL>::bytes(L) : 4;
+  const bool wpl = a.pot.w_planes != nullptr, rpl = TRWP && a.pot.rho_planes != nullptr;
+  const float g0 = a.desc->g[0], g1 = a.desc->g[1], g2 = a.desc->g[2];
+  float wg0 = fmul(a.pot.w, g0), wg1 = fmul(a.pot.w, g1), c = fmul(a.pot.w, g2);
+
+  for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
+    const LineDesc ld = a.lines[li];
+    const int r = ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
+    const int nsteps = ld.length - 1;
+    const float* rowp[ROWS];
+    rowp[0] = un + l0;
+#pragma unroll
+    for (int rr = 1; rr < ROWS; ++rr) {
+      const int idx = rr - 1;
+      const int d = TRWP ? (idx < r ? idx : idx + 1) : (idx < (r & ~1) ? idx : idx + 2);
+      rowp[rr] = a.m_in + img + size_t(d) * N * L + l0;
+    }
+    const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
+    const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
+    auto issue = [&](int j) {
+      const int slot = (j - 1) % kStages;
+      const int prev = ld.first + (j - 1) * st;
+      const size_t off = size_t(prev) * L;
+      if (FULL || nvalid > 0) {
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr)
+          cp_slice<EPL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid, chunk);
+      }
+      const int wnode = (r & 1) ? prev + st : prev;
+      if (wpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + lane), wrow + wnode, 4);
+      if (rpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + 32 + lane), rrow + wnode, 4);
+    };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+      if (1 + s <= nsteps) issue(1 + s);
+      cp_commit();
+    }
+    const size_t pq_base = (size_t(b) * g.K_cap + a.k) * g.E + g.dir_offset[r] + ld.edge_base;
+    float* mout = a.m_out + img + size_t(r) * N * L;
+    float carry[EPL];
+#pragma unroll
+    for (int i = 0; i < EPL; ++i) carry[i] = 0.0f;
+
+    for (int j = 1; j <= nsteps; ++j) {
+      if (j + kStages - 1 <= nsteps) issue(j + kStages - 1);
+      cp_commit();
+      cp_wait<kStages - 1>();
+      const int slot = (j - 1) % kStages;
+      const float* srow = ring + slot * ROWS * LS + l0;
+      if (wpl) {
+        const float w = s_x[slot * 64 + lane];
+        wg0 = fmul(w, g0), wg1 = fmul(w, g1), c = fmul(w, g2);
+      }
+
+      // ---- base (isgmr.hpp:82-88 / trwp.hpp:84-90 addition order)
+      float base[EPL];
+      {
+        float t[EPL];
+        lds_slice<EPL>(t, srow);
+        if (!TRWP) {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) base[i] = fadd(t[i], carry[i]);
+#pragma unroll
+          for (int rr = 1; rr < ROWS; ++rr) {
+            lds_slice<EPL>(t, srow + rr * LS);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) base[i] = fadd(base[i], t[i]);
+          }
+        } else {
+          const float rho = rpl ? s_x[slot * 64 + 32 + lane] : a.pot.rho;
+          float s[EPL], mo[EPL];
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) s[i] = t[i], mo[i] = 0.0f;
+#pragma unroll
+          for (int d = 0; d < R; ++d) {
+            lds_slice<EPL>(t, srow + (d < r ? d + 1 : d) * LS);  // d == r: unused read
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) {
+              const float x = d == r ? carry[i] : t[i];
+              mo[i] = d == opp ? t[i] : mo[i];
+              s[i] = fadd(s[i], x);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) base[i] = fsub(fmul(rho, s[i]), mo[i]);
+        }
+      }
+      if (!FULL) {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) base[i] = i < nvalid ? base[i] : kInf;
+      }
+
+      // ---- far-candidate cost, prefix / suffix (value, first index) scans
+      float u[EPL], pv[EPL], sv[EPL];
+      int pi[EPL], si[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) u[i] = fadd(base[i], c);
+      pv[0] = u[0];
+      pi[0] = l0;
+#pragma unroll
+      for (int i = 1; i < EPL; ++i) {
+        const bool t = u[i] < pv[i - 1];
+        pv[i] = t ? u[i] : pv[i - 1];
+        pi[i] = t ? l0 + i : pi[i - 1];
+      }
+      sv[EPL - 1] = u[EPL - 1];
+      si[EPL - 1] = l0 + EPL - 1;
+#pragma unroll
+      for (int i = EPL - 2; i >= 0; --i) {
+        const bool t = sv[i + 1] < u[i];
+        sv[i] = t ? sv[i + 1] : u[i];
+        si[i] = t ? si[i + 1] : l0 + i;
+      }
+      {
+        float tpv = pv[EPL - 1], tsv = sv[0];
+        int tpi = pi[EPL - 1], tsi = si[0];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const float opv = __shfl_up_sync(0xffffffffu, tpv, off);
+          const int opi = __shfl_up_sync(0xffffffffu, tpi, off);
+          const float osv = __shfl_down_sync(0xffffffffu, tsv, off);
+          const int osi = __shfl_down_sync(0xffffffffu, tsi, off);
+          const bool tp = lane >= off && !(tpv < opv);
+          const bool ts = lane + off < 32 && osv < tsv;
+          tpv = tp ? opv : tpv;
+          tpi = tp ? opi : tpi;
+          tsv = ts ? osv : tsv;
+          tsi = ts ? osi : tsi;
+        }
+        float epv = __shfl_up_sync(0xffffffffu, tpv, 1);
+        const int epi = __shfl_up_sync(0xffffffffu, tpi, 1);
+        float esv = __shfl_down_sync(0xffffffffu, tsv, 1);
+        const int esi = __shfl_down_sync(0xffffffffu, tsi, 1);
+        epv = lane > 0 ? epv : kInf;
+        esv = lane < 31 ? esv : kInf;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          const bool tp = !(pv[i] < epv);
+          pv[i] = tp ? epv : pv[i];
+          pi[i] = tp ? epi : pi[i];
+          const bool ts = esv < sv[i];
+          sv[i] = ts ? esv : sv[i];
+          si[i] = ts ? esi : si[i];
+        }
+      }
+
+      // ---- neighbours across lanes: base(l0-1), base(l0+EPL), far segment
+      // summaries at l-2 / l+2 for the lane's first / last two labels
+      float bl = __shfl_up_sync(0xffffffffu, base[EPL - 1], 1);
+      float br = __shfl_down_sync(0xffffffffu, base[0], 1);
+      bl = lane > 0 ? bl : kInf;
+      br = lane < 31 ? br : kInf;
+      constexpr int E2 = EPL >= 2 ? 2 : 1;  // labels per lane needing the neighbour's far summary
+      constexpr int SH = EPL >= 2 ? 1 : 2;  // lane distance of l-2 / l+2
+      float pvm[E2], svp[E2];
+      int pim[E2], sip[E2];
+#pragma unroll
+      for (int e = 0; e < E2; ++e) {
+        const int src_lo = EPL >= 2 ? EPL - 2 + e : 0;  // element l0 - 2 + e of lane - SH
+        const int src_hi = EPL >= 2 ? e : 0;            // element l0 + EPL + e of lane + SH
+        pvm[e] = __shfl_up_sync(0xffffffffu, pv[src_lo], SH);
+        pim[e] = __shfl_up_sync(0xffffffffu, pi[src_lo], SH);
+        svp[e] = __shfl_down_sync(0xffffffffu, sv[src_hi], SH);
+        sip[e] = __shfl_down_sync(0xffffffffu, si[src_hi], SH);
+        pvm[e] = lane >= SH ? pvm[e] : kInf;
+        svp[e] = lane + SH < 32 ? svp[e] : kInf;
+      }
+
+      // ---- combine in index order: [0,l-2] | l-1 | l | l+1 | [l+2,L)
+      float out[EPL];
+      int am[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int l = l0 + i;
+        const float lv = i >= 2 ? pv[i >= 2 ? i - 2 : 0] : pvm[i < E2 ? i : 0];
+        const int lix = i >= 2 ? pi[i >= 2 ? i - 2 : 0] : pim[i < E2 ? i : 0];
+        const float bm1 = i >= 1 ? base[i >= 1 ? i - 1 : 0] : bl;
+        const float bp1 = i + 1 < EPL ? base[i + 1 < EPL ? i + 1 : 0] : br;
+        const int hi = i + 2 - EPL;  // >= 0: right far summary lives in lane + SH
+        const float rv = hi < 0 ? sv[hi < 0 ? i + 2 : 0] : svp[hi >= 0 && hi < E2 ? hi : 0];
+        const int rix = hi < 0 ? si[hi < 0 ? i + 2 : 0] : sip[hi >= 0 && hi < E2 ? hi : 0];
+        float best = lv;
+        int arg = lv < kInf ? lix : 0;
+        float v = fadd(bm1, wg1);
+        bool t = v < best;
+        best = t ? v : best;
+        arg = t ? l - 1 : arg;
+        v = fadd(base[i], wg0);
+        t = v < best;
+        best = t ? v : best;
+        arg = t ? l : arg;
+        v = fadd(bp1, wg1);
+        t = v < best;
+        best = t ? v : best;
+        arg = t ? l + 1 : arg;
+        t = rv < best;
+        best = t ? rv : best;
+        arg = t ? rix : arg;
+        out[i] = (FULL || i < nvalid) ? best : kInf;
+        am[i] = arg;
+      }
+
+      // ---- p row, reparametrisation (first argmin; banded values are never -0)
+      store_p<EPL, FULL>(a.p + (pq_base + j - 1) * L, l0, am, nvalid);
+      uint32_t lk = order_key(out[0]);
+      int lidx = l0;
+#pragma unroll
+      for (int i = 1; i < EPL; ++i) {
+        const uint32_t kk = order_key(out[i]);
+        const bool t = kk < lk;
+        lk = t ? kk : lk;
+        lidx = t ? l0 + i : lidx;
+      }
+      const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
+      const uint32_t qmin = __reduce_min_sync(0xffffffffu, lk == kmin ? uint32_t(lidx) : 0xffffffffu);
+      const float lo = key_value(kmin);
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) carry[i] = fsub(out[i], lo);
+      const int cur = ld.first + j * st;
+      stg_slice<EPL>(mout + size_t(cur) * L, l0, carry, FULL ? EPL : nvalid, L);
+      if (lane == 0) a.q[pq_base + j - 1] = uint8_t(qmin);
+    }
+    cp_wait<0>();
+    __syncwarp();
+  }
+}
+
+}  // namespace mrf

@@ -38,7 +38,7 @@ struct PairDesc {
 // One block. Bit-level checks: symmetric Toeplitz, constant tail, and no -0
 // in the weight / rho planes (so no candidate value can be -0, which makes the
 // scanned minimum value equal to the first argmin's raw value).
-__global__ void analyze_pairwise_kernel(const float* __restrict__ V, int L, const float* __restrict__ wplanes,
+static __global__ void analyze_pairwise_kernel(const float* __restrict__ V, int L, const float* __restrict__ wplanes,
                                         int64_t nw, float wconst, const float* __restrict__ rplanes, int64_t nr,
                                         PairDesc* __restrict__ out) {
   int ok = 1;
@@ -74,6 +74,7 @@ struct FwdArgs {
   uint8_t* q;
   int k;
   const PairDesc* desc;
+  int band2_launched;  // fwd_band2_kernel covers banded D == 2 in this sweep
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {
@@ -503,8 +504,11 @@ __global__ void __launch_bounds__(128) fwd_warp_kernel(FwdArgs a) {
   const int rows = 1 + (TRWP ? R - 1 : R - 2);
   float* ws = smem + size_t(threadIdx.x >> 5) * fwd_warp_smem_floats(EPL, rows);
   if (a.desc->banded) {
-    if (a.desc->D == 2) fwd_sweep_lines<EPL, TRWP, 2>(a, ws);
-    else fwd_sweep_lines<EPL, TRWP, 1>(a, ws);
+    if (a.desc->D == 2) {
+      if (!a.band2_launched) fwd_sweep_lines<EPL, TRWP, 2>(a, ws);
+    } else {
+      fwd_sweep_lines<EPL, TRWP, 1>(a, ws);
+    }
   } else {
     fwd_sweep_lines<EPL, TRWP, 0>(a, ws);
   }

@@ -1,0 +1,30 @@
+// Kernel launchers, one translation unit per kernel family (compiled in
+// parallel). Each returns the CUDA error of its launch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "bwd_warp.cuh"
+#include "fwd_warp.cuh"
+
+namespace mrf {
+
+// labels per lane for the warp-per-scanline kernels
+inline int epl_for(int L) {
+  if (L <= 32) return 1;
+  if (L <= 64) return 2;
+  if (L <= 128) return 4;
+  if (L <= 192) return 6;
+  return 8;
+}
+
+// warps per CTA: few long chains -> spread them over every SM
+inline int warps_per_cta(int nlines) { return nlines >= 148 * 8 ? 4 : (nlines >= 148 * 2 ? 2 : 1); }
+
+cudaError_t launch_fwd_generic(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
+cudaError_t launch_fwd_band2_isgmr(const FwdArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_fwd_band2_trwp(const FwdArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_bwd(const BwdArgs& a, int batch, bool trwp, cudaStream_t s);
+
+
+}  // namespace mrf

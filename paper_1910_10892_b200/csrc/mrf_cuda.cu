@@ -15,8 +15,7 @@
 
 #include "../../include/mrf_cuda.h"
 #include "common.cuh"
-#include "fwd_warp.cuh"
-#include "bwd_warp.cuh"
+#include "launch.hpp"
 #include "kernels_v1.cuh"  // aggregate + broadcast helpers
 #include "topology.hpp"
 
@@ -249,43 +248,21 @@ class PairDescHolder {
   PairDesc* d_ = nullptr;
 };
 
-int epl_for(int L) {
-  if (L <= 32) return 1;
-  if (L <= 64) return 2;
-  if (L <= 128) return 4;
-  if (L <= 192) return 6;
-  return 8;
-}
-
-template <int EPL, bool TRWP>
-void launch_fwd_epl(const FwdArgs& a, int R, int batch, cudaStream_t stream) {
-  const int rows = 1 + (TRWP ? R - 1 : R - 2);
-  const int per_warp = fwd_warp_smem_floats(EPL, rows) * int(sizeof(float));
-  // few long chains (e.g. 375 rows of a KITTI frame) -> 1 warp per CTA so
-  // they spread over all SMs; many chains -> 4 warps per CTA
-  const int wpc = a.nlines >= 148 * 8 ? 4 : (a.nlines >= 148 * 2 ? 2 : 1);
-  const int smem = per_warp * wpc;
-  auto kern = fwd_warp_kernel<EPL, TRWP>;
-  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
-  const int blocks = std::min((a.nlines + wpc - 1) / wpc, 65535);
-  ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
-  kern<<<dim3(blocks, batch), 32 * wpc, smem, stream>>>(a);
-  cuda_check(cudaGetLastError(), "fwd_warp_kernel launch");
-}
-
 template <bool TRWP>
 void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines, int nlines,
                           const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k, const PairDesc* desc,
                           cudaStream_t stream) {
   if (nlines == 0) return;
-  FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc};
-  switch (epl_for(pr->labels)) {
-    case 1: launch_fwd_epl<1, TRWP>(a, g.R, pr->batch, stream); break;
-    case 2: launch_fwd_epl<2, TRWP>(a, g.R, pr->batch, stream); break;
-    case 4: launch_fwd_epl<4, TRWP>(a, g.R, pr->batch, stream); break;
-    case 6: launch_fwd_epl<6, TRWP>(a, g.R, pr->batch, stream); break;
-    default: launch_fwd_epl<8, TRWP>(a, g.R, pr->batch, stream); break;
-  }
+  // The pairwise strategy is only known on the device (desc), so the banded
+  // D == 2 specialisation and the generic kernel are both launched; each
+  // returns at once when the other one owns the sweep.
+  const bool band2 = g.R == 4 || g.R == 8;
+  FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0};
+  ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
+  if (band2)
+    cuda_check(TRWP ? launch_fwd_band2_trwp(a, pr->batch, stream) : launch_fwd_band2_isgmr(a, pr->batch, stream),
+               "fwd_band2_kernel launch");
+  cuda_check(launch_fwd_generic(a, pr->batch, TRWP, stream), "fwd_warp_kernel launch");
 }
 
 void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* messages, float* cost, uint16_t* labels,
@@ -322,30 +299,11 @@ size_t gvacc_bytes(const mrf_problem_f32* pr) {
   return sizeof(float) * size_t(pr->batch) * kVRep * 2 * pr->labels * pr->labels;
 }
 
-template <int EPL, bool TRWP>
-void launch_bwd_epl(const BwdArgs& a, int R, int batch, cudaStream_t stream) {
-  const int rowsF = 2 + (TRWP ? R - 1 : R - 2);
-  const int per_warp = bwd_warp_smem_floats(EPL, rowsF) * int(sizeof(float));
-  const int wpc = a.nlines >= 148 * 8 ? 4 : (a.nlines >= 148 * 2 ? 2 : 1);
-  const int smem = per_warp * wpc;
-  auto kern = bwd_warp_kernel<EPL, TRWP>;
-  cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "cudaFuncSetAttribute");
-  const int blocks = std::min((a.nlines + wpc - 1) / wpc, 65535);
-  ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
-  kern<<<dim3(blocks, batch), 32 * wpc, smem, stream>>>(a);
-  cuda_check(cudaGetLastError(), "bwd_warp_kernel launch");
-}
-
 template <bool TRWP>
-void launch_backward_sweep(const BwdArgs& a, int L, int R, int batch, cudaStream_t stream) {
+void launch_backward_sweep(const BwdArgs& a, int batch, cudaStream_t stream) {
   if (a.nlines == 0) return;
-  switch (epl_for(L)) {
-    case 1: launch_bwd_epl<1, TRWP>(a, R, batch, stream); break;
-    case 2: launch_bwd_epl<2, TRWP>(a, R, batch, stream); break;
-    case 4: launch_bwd_epl<4, TRWP>(a, R, batch, stream); break;
-    case 6: launch_bwd_epl<6, TRWP>(a, R, batch, stream); break;
-    default: launch_bwd_epl<8, TRWP>(a, R, batch, stream); break;
-  }
+  ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
+  cuda_check(launch_bwd(a, batch, TRWP, stream), "bwd_warp_kernel launch");
 }
 
 template <bool TRWP>
@@ -386,7 +344,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
                 gm, gnext, grads->unary, grads->weight_planes, gvacc};
       // plane r of gm is consumed and left zero by the sweep (the reference's
       // plane clear, autodiff.hpp:190-193, and swap-and-clear, :122-123)
-      launch_backward_sweep<TRWP>(a, L, R, B, stream);
+      launch_backward_sweep<TRWP>(a, B, stream);
     }
     if (!TRWP) std::swap(gm, gnext);
   }
