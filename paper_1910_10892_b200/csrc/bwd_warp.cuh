@@ -17,9 +17,11 @@
 // owned by exactly one warp within a launch (scanlines of one direction are
 // node-disjoint), so dtheta / gm / dw need no atomics and are deterministic;
 // dV partials use fire-and-forget reductions (RED) into a few replicas
-// (near-diagonal ones accumulate in registers first). The rows a step
-// touches do not depend on the chain and are prefetched with cp.async
-// kStages-1 steps ahead, as in the forward.
+// (near-diagonal ones accumulate in registers over the whole sweep). The
+// per-edge dw sums are deferred: lane partials of 32 consecutive edges are
+// parked in shared memory and reduced together. The rows a step touches do
+// not depend on the chain and are prefetched with cp.async kStages-1 steps
+// ahead, as in the forward.
 #pragma once
 
 #include "common.cuh"
@@ -47,8 +49,9 @@ struct BwdArgs {
 
 // per-warp ring stage: rowsF float rows + p words + {q, w, rho} words per lane
 __host__ __device__ constexpr int bwd_stage_floats(int EPL, int rowsF) { return rowsF * 32 * EPL + 8 * EPL + 4 + 96; }
+// ring + dw parking [32][33]
 __host__ __device__ constexpr int bwd_warp_smem_floats(int EPL, int rowsF) {
-  return (kStages * bwd_stage_floats(EPL, rowsF) + 31) / 32 * 32;
+  return (kStages * bwd_stage_floats(EPL, rowsF) + 32 * 33 + 31) / 32 * 32;
 }
 
 __device__ __forceinline__ float warp_sum_f(float v) {
@@ -58,7 +61,8 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 }
 
 // RT: compile-time direction count (4 or 8), or 0 for runtime R.
-template <int EPL, bool TRWP, int RT>
+// FULL: L == 32*EPL (every lane owns EPL valid labels).
+template <int EPL, bool TRWP, int RT, bool FULL>
 __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   extern __shared__ float smem[];
   const Geometry& g = a.g;
@@ -71,16 +75,18 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   constexpr int LS = 32 * EPL;
   const int stage_f = bwd_stage_floats(EPL, rowsF);
   float* ring = smem + size_t(wid) * bwd_warp_smem_floats(EPL, rowsF);
+  float* s_wp = ring + kStages * stage_f;  // [32][33] parked dw lane partials
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
 
   const int b = blockIdx.y;
   const size_t img = size_t(b) * R * N * L;
-  float* gmr = a.gm + img + size_t(r) * N * L;
-  float* gub = a.gu + size_t(b) * N * L;
+  const size_t NL = size_t(N) * L;
+  float* gmr = a.gm + img + size_t(r) * NL;
+  float* gub = a.gu + size_t(b) * NL;
   float* planes_base = TRWP ? a.gm + img : a.gnext + img;
   const int l0 = lane * EPL;
-  const int nvalid = min(EPL, max(0, L - l0));
-  const int chunk = nvalid == EPL ? Chunk<EPL>::bytes(L) : 4;
+  const int nvalid = FULL ? EPL : min(EPL, max(0, L - l0));
+  const int chunk = (FULL || nvalid == EPL) ? Chunk<EPL>::bytes(L) : 4;
   const bool wpl = a.pot.w_planes != nullptr, rpl = TRWP && a.pot.rho_planes != nullptr;
   const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
   const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
@@ -88,10 +94,25 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   float* gvacc = a.gvacc + ((size_t(b) * kVRep + warp_global % kVRep) * 2 + (r & 1)) * L * L;
   const bool do_w = a.gw != nullptr;
   float* gwrow = do_w ? a.gw + (size_t(b) * (R / 2) + fam) * N : nullptr;
-  // plane rows at prev, ascending d: TRWP skips r, ISGMR skips {r, r^1}
-  auto plane_of = [&](int idx) { return TRWP ? (idx < r ? idx : idx + 1) : (idx < (r & ~1) ? idx : idx + 2); };
+  // plane offsets at a node, ascending d: TRWP skips r, ISGMR skips {r, r^1}
+  size_t poff[RT ? (TRWP ? RT - 1 : RT - 2) : 15];
+#pragma unroll
+  for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr) {
+    const int d = TRWP ? (rr < r ? rr : rr + 1) : (rr < (r & ~1) ? rr : rr + 2);
+    poff[rr] = size_t(d) * NL + l0;
+  }
+  // near-diagonal V'(l + delta, l), delta = -1, 0, 1 (for dw), per direction parity
+  float vloc[EPL][3];
+#pragma unroll
+  for (int i = 0; i < EPL; ++i)
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int l = l0 + i, mu = l + t - 1;
+      const bool ok = do_w && l < L && mu >= 0 && mu < L;
+      vloc[i][t] = ok ? __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+    }
 
-  float vacc[EPL][3];  // near-diagonal dV partials, (mu = l + delta, l), delta = -1, 0, 1
+  float vacc[EPL][3];  // near-diagonal dV partials, (mu = l + delta, l)
 #pragma unroll
   for (int i = 0; i < EPL; ++i) vacc[i][0] = vacc[i][1] = vacc[i][2] = 0.0f;
   float zero[EPL];
@@ -109,13 +130,13 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       const uint32_t base_s = ring_s + 4u * uint32_t(slot * stage_f);
       const int j = nsteps - s;
       const int cur = ld.first + j * st, prev = cur - st;
-      if (nvalid > 0) {
+      if (FULL || nvalid > 0) {
+        const size_t pn = size_t(prev) * L;
         cp_slice<EPL>(base_s + 4u * l0, gmr + size_t(cur) * L + l0, nvalid, chunk);
-        cp_slice<EPL>(base_s + 4u * (LS + l0), gub + size_t(prev) * L + l0, nvalid, chunk);
-#pragma unroll 4
-        for (int rr = 0; rr < NP; ++rr)
-          cp_slice<EPL>(base_s + 4u * ((2 + rr) * LS + l0), planes_base + (size_t(plane_of(rr)) * N + prev) * L + l0,
-                        nvalid, chunk);
+        cp_slice<EPL>(base_s + 4u * (LS + l0), gub + pn + l0, nvalid, chunk);
+#pragma unroll
+        for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr)
+          if (RT || rr < NP) cp_slice<EPL>(base_s + 4u * ((2 + rr) * LS + l0), planes_base + poff[rr] + pn, nvalid, chunk);
       }
       // p row: the aligned words covering bytes [flat*L, flat*L + L)
       const size_t flat = pq_base + j - 1;
@@ -130,6 +151,20 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       const int wnode = (r & 1) ? cur : prev;
       if (wpl) cp_async_u32(xdst + 4u * (32 + lane), wrow + wnode, 4);
       if (rpl) cp_async_u32(xdst + 4u * (64 + lane), rrow + wnode, 4);
+    };
+    // deferred per-edge dw: reduce parked lane partials of steps [s0, s0+cnt)
+    auto flush_w = [&](int s0, int cnt) {
+      __syncwarp();
+      if (lane < cnt) {
+        float t = 0.0f;
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) t = fadd(t, s_wp[lane * 33 + c]);
+        const int j = nsteps - (s0 + lane);
+        const int cur = ld.first + j * st;
+        float* dst = gwrow + ((r & 1) ? cur : cur - st);
+        *dst = fadd(*dst, t);
+      }
+      __syncwarp();
     };
 
 #pragma unroll
@@ -150,7 +185,7 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       const int j = nsteps - s;
       const int cur = ld.first + j * st, prev = cur - st;
       const size_t flat = pq_base + j - 1;
-      const uint8_t* prow = reinterpret_cast<const uint8_t*>(slot + rowsF * LS) + ((flat * L) & 3);
+      const uint8_t* prow = reinterpret_cast<const uint8_t*>(slot + rowsF * LS) + ((flat * L) & 3) + l0;
       const float* xs = slot + rowsF * LS + 8 * EPL + 4;
       const int qv = (__float_as_uint(xs[lane]) >> (8 * (flat & 3))) & 0xff;
       const float w = wpl ? xs[32 + lane] : a.pot.w;
@@ -158,30 +193,44 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
 
       // ---- row = gm^r[cur] + carry; consume (zero) gm^r[cur]; reparam backward
       float row[EPL];
+      int pm[EPL];
       {
         float t[EPL];
         lds_slice<EPL>(t, slot + l0);
         float lsum = 0.0f;
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
-          row[i] = i < nvalid ? fadd(t[i], carry[i]) : 0.0f;
+          row[i] = (FULL || i < nvalid) ? fadd(t[i], carry[i]) : 0.0f;
           lsum = fadd(lsum, row[i]);
+          pm[i] = (FULL || i < nvalid) ? int(prow[i]) : 0;
         }
         stg_slice<EPL>(gmr + size_t(cur) * L, l0, zero, nvalid, L);
         const float S = warp_sum_f(lsum);
 #pragma unroll
         for (int i = 0; i < EPL; ++i) row[i] = l0 + i == qv ? fsub(row[i], S) : row[i];
       }
-      int pm[EPL];
+      bool live[EPL];
+      int dl[EPL];
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) pm[i] = i < nvalid ? int(prow[l0 + i]) : 0;
+      for (int i = 0; i < EPL; ++i) {
+        live[i] = (FULL || i < nvalid) && row[i] != 0.0f;
+        dl[i] = pm[i] - (l0 + i);
+      }
+      // far targets' V' values, issued early so their latency overlaps the scatter
+      float vfar[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int l = l0 + i, mu = pm[i];
+        const bool far = do_w && live[i] && (dl[i] < -1 || dl[i] > 1);
+        vfar[i] = far ? __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+      }
 
       // ---- scatter: acc[mu] = sum over l with p[l] = mu of g_l
       float acc[EPL];
 #pragma unroll
       for (int i = 0; i < EPL; ++i) acc[i] = 0.0f;
       if (EPL == 1) {
-        const float g0 = row[0];
+        const float g0 = live[0] ? row[0] : 0.0f;
 #pragma unroll 8
         for (int lam = 0; lam < L; ++lam) {
           const int pl = __shfl_sync(0xffffffffu, pm[0], lam);
@@ -194,18 +243,19 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
           const float gi = row[i];
-          const bool live = i < nvalid && gi != 0.0f;
-          const int d = pm[i] - (l0 + i);
-          if (live && d == 0) acc[i] = fadd(acc[i], gi);
-          if (live && d == -1) {
-            if (i > 0) acc[i > 0 ? i - 1 : 0] = fadd(acc[i > 0 ? i - 1 : 0], gi);
-            else accL = fadd(accL, gi);
+          acc[i] = live[i] && dl[i] == 0 ? fadd(acc[i], gi) : acc[i];
+          if (i > 0) {
+            acc[i > 0 ? i - 1 : 0] = live[i] && dl[i] == -1 ? fadd(acc[i > 0 ? i - 1 : 0], gi) : acc[i > 0 ? i - 1 : 0];
+          } else {
+            accL = live[i] && dl[i] == -1 ? fadd(accL, gi) : accL;
           }
-          if (live && d == 1) {
-            if (i + 1 < EPL) acc[i + 1 < EPL ? i + 1 : 0] = fadd(acc[i + 1 < EPL ? i + 1 : 0], gi);
-            else accR = fadd(accR, gi);
+          if (i + 1 < EPL) {
+            acc[i + 1 < EPL ? i + 1 : 0] =
+                live[i] && dl[i] == 1 ? fadd(acc[i + 1 < EPL ? i + 1 : 0], gi) : acc[i + 1 < EPL ? i + 1 : 0];
+          } else {
+            accR = live[i] && dl[i] == 1 ? fadd(accR, gi) : accR;
           }
-          rem[i] = live && (d < -1 || d > 1);
+          rem[i] = live[i] && (dl[i] < -1 || dl[i] > 1);
         }
         const float fromR = __shfl_down_sync(0xffffffffu, accL, 1);
         const float fromL = __shfl_up_sync(0xffffffffu, accR, 1);
@@ -215,18 +265,14 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
         // target are summed with two independent warp reductions
         while (true) {
           uint32_t mn = 0xffffffffu, mx = 0u;
-          bool any = false;
 #pragma unroll
-          for (int i = 0; i < EPL; ++i)
-            if (rem[i]) {
-              mn = min(mn, uint32_t(pm[i]));
-              mx = max(mx, uint32_t(pm[i]) + 1u);
-              any = true;
-            }
+          for (int i = 0; i < EPL; ++i) {
+            mn = rem[i] ? min(mn, uint32_t(pm[i])) : mn;
+            mx = rem[i] ? max(mx, uint32_t(pm[i]) + 1u) : mx;
+          }
           const uint32_t kmin = __reduce_min_sync(0xffffffffu, mn);
           if (kmin == 0xffffffffu) break;
           const uint32_t kmax = __reduce_max_sync(0xffffffffu, mx) - 1u;
-          (void)any;
           float pa = 0.0f, pb2 = 0.0f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
@@ -243,64 +289,57 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
           }
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
-            if (int(kmin) == l0 + i) acc[i] = fadd(acc[i], pa);
-            if (kmax != kmin && int(kmax) == l0 + i) acc[i] = fadd(acc[i], pb2);
+            acc[i] = int(kmin) == l0 + i ? fadd(acc[i], pa) : acc[i];
+            acc[i] = (kmax != kmin && int(kmax) == l0 + i) ? fadd(acc[i], pb2) : acc[i];
           }
         }
       }
 
-      // ---- dw and dV contributions of this edge
+      // ---- apply to the predecessor rows; carry the own-plane share
+      {
+        float outv[EPL], t[EPL], add[EPL];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) add[i] = TRWP ? fmul(rho, acc[i]) : acc[i];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) carry[i] = add[i];
+        const size_t pn = size_t(prev) * L;
+        lds_slice<EPL>(t, slot + LS + l0);
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) outv[i] = fadd(t[i], add[i]);
+        stg_slice<EPL>(gub + pn, l0, outv, nvalid, L);
+#pragma unroll
+        for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr) {
+          if (RT || rr < NP) {
+            const bool is_opp = TRWP && (rr < r ? rr : rr + 1) == opp;
+            lds_slice<EPL>(t, slot + (2 + rr) * LS + l0);
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) {
+              const float v = fadd(t[i], add[i]);
+              outv[i] = is_opp ? fsub(v, acc[i]) : v;
+            }
+            stg_slice<EPL>(planes_base + poff[rr] - l0 + pn, l0, outv, nvalid, L);
+          }
+        }
+      }
+
+      // ---- dw (parked) and dV contributions of this edge
       float wpart = 0.0f;
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         const float gi = row[i];
-        const bool live = i < nvalid && gi != 0.0f;
-        const int l = l0 + i, mu = pm[i];
-        if (do_w && live) {
-          const float vv = __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l));
-          wpart = fadd(wpart, fmul(gi, vv));
-        }
+        const int d = dl[i];
+        const float vv = d == -1 ? vloc[i][0] : d == 0 ? vloc[i][1] : d == 1 ? vloc[i][2] : vfar[i];
+        wpart = live[i] ? fadd(wpart, fmul(gi, vv)) : wpart;
         const float gwv = fmul(gi, w);
-        const int d = mu - l;
-        vacc[i][0] = live && d == -1 ? fadd(vacc[i][0], gwv) : vacc[i][0];
-        vacc[i][1] = live && d == 0 ? fadd(vacc[i][1], gwv) : vacc[i][1];
-        vacc[i][2] = live && d == 1 ? fadd(vacc[i][2], gwv) : vacc[i][2];
-        if (live && (d < -1 || d > 1)) atomicAdd(gvacc + size_t(mu) * L + l, gwv);
+        vacc[i][0] = live[i] && d == -1 ? fadd(vacc[i][0], gwv) : vacc[i][0];
+        vacc[i][1] = live[i] && d == 0 ? fadd(vacc[i][1], gwv) : vacc[i][1];
+        vacc[i][2] = live[i] && d == 1 ? fadd(vacc[i][2], gwv) : vacc[i][2];
+        if (live[i] && (d < -1 || d > 1)) atomicAdd(gvacc + size_t(pm[i]) * L + l0 + i, gwv);
       }
       if (do_w) {
-        const float wsum = warp_sum_f(wpart);
-        if (lane == 0) {
-          float* t = gwrow + ((r & 1) ? cur : prev);
-          *t = fadd(*t, wsum);
-        }
+        s_wp[(s & 31) * 33 + lane] = wpart;
+        if ((s & 31) == 31 || s == nsteps - 1) flush_w(s & ~31, (s & 31) + 1);
       }
-
-      // ---- apply to the predecessor rows
-      float outv[EPL], t[EPL], add[EPL];
-      if (!TRWP) {
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) add[i] = acc[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) add[i] = fmul(rho, acc[i]);
-      }
-      lds_slice<EPL>(t, slot + LS + l0);
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) outv[i] = fadd(t[i], add[i]);
-      stg_slice<EPL>(gub + size_t(prev) * L, l0, outv, nvalid, L);
-#pragma unroll 4
-      for (int rr = 0; rr < NP; ++rr) {
-        const int d = plane_of(rr);
-        lds_slice<EPL>(t, slot + (2 + rr) * LS + l0);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) {
-          const float v = fadd(t[i], add[i]);
-          outv[i] = (TRWP && d == opp) ? fsub(v, acc[i]) : v;
-        }
-        stg_slice<EPL>(planes_base + (size_t(d) * N + prev) * L, l0, outv, nvalid, L);
-      }
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) carry[i] = add[i];
       __syncwarp();
     }
     // head row of plane r: its incoming scatter (carry) is dropped and the row
@@ -313,11 +352,10 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
 #pragma unroll
   for (int i = 0; i < EPL; ++i) {
     const int l = l0 + i;
-    if (i >= nvalid) continue;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const int mu = l + t - 1;
-      if (mu >= 0 && mu < L && vacc[i][t] != 0.0f) atomicAdd(gvacc + size_t(mu) * L + l, vacc[i][t]);
+      if (l < L && mu >= 0 && mu < L && vacc[i][t] != 0.0f) atomicAdd(gvacc + size_t(mu) * L + l, vacc[i][t]);
     }
   }
 }

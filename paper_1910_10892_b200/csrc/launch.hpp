@@ -24,7 +24,8 @@ inline int warps_per_cta(int nlines) { return nlines >= 148 * 8 ? 4 : (nlines >=
 cudaError_t launch_fwd_generic(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 cudaError_t launch_fwd_band2_isgmr(const FwdArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_fwd_band2_trwp(const FwdArgs& a, int batch, cudaStream_t s);
-cudaError_t launch_bwd(const BwdArgs& a, int batch, bool trwp, cudaStream_t s);
+cudaError_t launch_bwd_isgmr(const BwdArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_bwd_trwp(const BwdArgs& a, int batch, cudaStream_t s);
 
 
 }  // namespace mrf

@@ -303,7 +303,7 @@ template <bool TRWP>
 void launch_backward_sweep(const BwdArgs& a, int batch, cudaStream_t stream) {
   if (a.nlines == 0) return;
   ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
-  cuda_check(launch_bwd(a, batch, TRWP, stream), "bwd_warp_kernel launch");
+  cuda_check(TRWP ? launch_bwd_trwp(a, batch, stream) : launch_bwd_isgmr(a, batch, stream), "bwd_warp_kernel launch");
 }
 
 template <bool TRWP>
