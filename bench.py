@@ -271,14 +271,14 @@ def main():
         if world > 1:
             dist.barrier()
 
+    clocks = ClockSampler(local)  # sampling from warm-up through the timed region
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
-    clocks.start()
     _lib.check(_lib.lib().mrf_profiler_enable(1))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)

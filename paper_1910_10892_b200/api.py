@@ -183,17 +183,34 @@ def _alloc_forward(mrf: MRF, K: int):
         iterations=K)
 
 
+_WS: dict = {}
+
+
+def _workspace(kind: str, nbytes: int, device, stream):
+    """Per-(device, stream, kind) workspace reused across calls. Calls on one
+    stream are ordered, so reuse is safe; it grows when a larger one is
+    needed (the old buffer is released only after the stream drains it)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (str(device), s.cuda_stream, kind)
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        if buf is not None:
+            buf.record_stream(s)
+        buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf
+
+
 def _forward(engine: int, mrf: MRF, K: int, out: ForwardResult | None, stream):
     if K < 1:
         raise _lib.MrfInvalidArgument(1, "iterations must be >= 1")
     out = out or _alloc_forward(mrf, K)
     pr = mrf.c_problem()
     wsb = lib().mrf_forward_workspace_bytes(mrf.topo.handle, C.byref(pr), engine, K)
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=mrf.unary.device)
+    ws = _workspace("fwd", wsb, mrf.unary.device, stream)
     fo = _lib.ForwardOut(_ptr(out.cost), _ptr(out.labels), _ptr(out.messages), _ptr(out.p), _ptr(out.q))
     fn = lib().mrf_isgmr_forward_f32 if engine == ENGINE_ISGMR else lib().mrf_trwp_forward_f32
     check(fn(mrf.topo.handle, C.byref(pr), K, C.byref(fo), _ptr(ws), wsb, _stream(stream)))
-    out._workspace = ws  # keep alive until the stream consumes it
     return out
 
 
@@ -217,12 +234,11 @@ def _backward(engine: int, mrf: MRF, fwd_p, fwd_q, K: int, grad_cost, out: Gradi
                              torch.empty((B, t.num_dirs // 2, t.nodes), dtype=torch.float32, device=dev))
     pr = mrf.c_problem()
     wsb = lib().mrf_backward_workspace_bytes(t.handle, C.byref(pr), engine, K)
-    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    ws = _workspace("bwd", wsb, dev, stream)
     g = _lib.Grads(_ptr(out.unary), _ptr(out.pairwise), _ptr(out.edge_weights))
     fn = lib().mrf_isgmr_backward_f32 if engine == ENGINE_ISGMR else lib().mrf_trwp_backward_f32
     check(fn(t.handle, C.byref(pr), K, _ptr(fwd_p), _ptr(fwd_q), _ptr(grad_cost), C.byref(g), _ptr(ws), wsb,
              _stream(stream)))
-    out._workspace = ws
     return out
 
 

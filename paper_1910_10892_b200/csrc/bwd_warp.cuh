@@ -86,7 +86,6 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   float* planes_base = TRWP ? a.gm + img : a.gnext + img;
   const int l0 = lane * EPL;
   const int nvalid = FULL ? EPL : min(EPL, max(0, L - l0));
-  const int chunk = (FULL || nvalid == EPL) ? Chunk<EPL>::bytes(L) : 4;
   const bool wpl = a.pot.w_planes != nullptr, rpl = TRWP && a.pot.rho_planes != nullptr;
   const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
   const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
@@ -132,11 +131,11 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       const int cur = ld.first + j * st, prev = cur - st;
       if (FULL || nvalid > 0) {
         const size_t pn = size_t(prev) * L;
-        cp_slice<EPL>(base_s + 4u * l0, gmr + size_t(cur) * L + l0, nvalid, chunk);
-        cp_slice<EPL>(base_s + 4u * (LS + l0), gub + pn + l0, nvalid, chunk);
+        cp_slice_t<EPL, FULL>(base_s + 4u * l0, gmr + size_t(cur) * L + l0, nvalid);
+        cp_slice_t<EPL, FULL>(base_s + 4u * (LS + l0), gub + pn + l0, nvalid);
 #pragma unroll
         for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr)
-          if (RT || rr < NP) cp_slice<EPL>(base_s + 4u * ((2 + rr) * LS + l0), planes_base + poff[rr] + pn, nvalid, chunk);
+          if (RT || rr < NP) cp_slice_t<EPL, FULL>(base_s + 4u * ((2 + rr) * LS + l0), planes_base + poff[rr] + pn, nvalid);
       }
       // p row: the aligned words covering bytes [flat*L, flat*L + L)
       const size_t flat = pq_base + j - 1;

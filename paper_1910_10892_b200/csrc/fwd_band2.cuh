@@ -58,7 +58,6 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   const size_t img = size_t(b) * R * N * L;
   const int l0 = lane * EPL;
   const int nvalid = FULL ? EPL : min(EPL, max(0, L - l0));
-  const int chunk = (FULL || nvalid == EPL) ? Chunk<EPL>::bytes(L) : 4;
   const bool wpl = a.pot.w_planes != nullptr, rpl = TRWP && a.pot.rho_planes != nullptr;
   const float g0 = a.desc->g[0], g1 = a.desc->g[1], g2 = a.desc->g[2];
   float wg0 = fmul(a.pot.w, g0), wg1 = fmul(a.pot.w, g1), c = fmul(a.pot.w, g2);
@@ -84,7 +83,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       if (FULL || nvalid > 0) {
 #pragma unroll
         for (int rr = 0; rr < ROWS; ++rr)
-          cp_slice<EPL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid, chunk);
+          cp_slice_t<EPL, FULL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid);
       }
       const int wnode = (r & 1) ? prev + st : prev;
       if (wpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + lane), wrow + wnode, 4);

@@ -123,6 +123,23 @@ __device__ __forceinline__ void cp_slice(uint32_t saddr, const float* src, int n
   }
 }
 
+// Compile-time variant: FULL slices (L == 32*EPL, so rows are 16 B aligned)
+// use the widest chunk the slice allows; otherwise 4 B copies of the valid
+// elements. No runtime chunk selection (which would be predicated into both
+// instruction sequences).
+template <int EPL, bool FULL>
+__device__ __forceinline__ void cp_slice_t(uint32_t saddr, const float* src, int nvalid) {
+  if (FULL) {
+    constexpr int CH = EPL % 4 == 0 ? 16 : (EPL % 2 == 0 ? 8 : 4);
+#pragma unroll
+    for (int c = 0; c < EPL * 4 / CH; ++c) cp_async_u32(saddr + CH * c, src + (CH / 4) * c, CH);
+  } else {
+#pragma unroll
+    for (int c = 0; c < EPL; ++c)
+      if (c < nvalid) cp_async_u32(saddr + 4 * c, src + c, 4);
+  }
+}
+
 // Read a lane's EPL floats from shared memory (vectorised when aligned).
 template <int EPL>
 __device__ __forceinline__ void lds_slice(float (&v)[EPL], const float* s) {
