@@ -11,7 +11,7 @@ static cudaError_t run(const BwdArgs& a, int batch, cudaStream_t s) {
   const int wpc = warps_per_cta(a.nlines);
   const int smem = bwd_warp_smem_floats(EPL, rowsF) * int(sizeof(float)) * wpc;
   auto kern = bwd_warp_kernel<EPL, true, RT, FULL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
   kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);

@@ -21,7 +21,8 @@
 // per-edge dw sums are deferred: lane partials of 32 consecutive edges are
 // parked in shared memory and reduced together. The rows a step touches do
 // not depend on the chain and are prefetched with cp.async kStages-1 steps
-// ahead, as in the forward.
+// ahead, as in the forward. All in-image addressing is 32-bit (the host
+// rejects images with R*N*L >= 2^31 floats or K*E*L >= 2^32 index bytes).
 #pragma once
 
 #include "common.cuh"
@@ -45,6 +46,7 @@ struct BwdArgs {
   float* gu;     // [B][N][L]
   float* gw;     // [B][R/2][N] or null
   float* gvacc;  // [B][kVRep][2][L][L]
+  const PairDesc* desc;  // banded V: V'(mu, l) = g(min(|mu - l|, D)) without a table load
 };
 
 // per-warp ring stage: rowsF float rows + p words + {q, w, rho} words per lane
@@ -65,6 +67,8 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 template <int EPL, bool TRWP, int RT, bool FULL>
 __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   extern __shared__ float smem[];
+  constexpr int NPMAX = RT ? (TRWP ? RT - 1 : RT - 2) : 15;
+  constexpr int LS = 32 * EPL;
   const Geometry& g = a.g;
   const int L = g.L, N = g.N;
   const int R = RT ? RT : g.R;
@@ -72,18 +76,20 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   const int r = a.r, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
   const int NP = TRWP ? R - 1 : R - 2;
   const int rowsF = 2 + NP;  // gm^r[cur], dtheta[prev], NP gradient planes at prev
-  constexpr int LS = 32 * EPL;
   const int stage_f = bwd_stage_floats(EPL, rowsF);
   float* ring = smem + size_t(wid) * bwd_warp_smem_floats(EPL, rowsF);
   float* s_wp = ring + kStages * stage_f;  // [32][33] parked dw lane partials
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
 
   const int b = blockIdx.y;
-  const size_t img = size_t(b) * R * N * L;
-  const size_t NL = size_t(N) * L;
-  float* gmr = a.gm + img + size_t(r) * NL;
-  float* gub = a.gu + size_t(b) * NL;
-  float* planes_base = TRWP ? a.gm + img : a.gnext + img;
+  const int NL = N * L;
+  const int stL = st * L;
+  float* img_gm = a.gm + size_t(b) * R * NL;
+  float* gmr = img_gm + r * NL + lane * EPL;  // lane slice of plane r, node 0
+  float* gub = a.gu + size_t(b) * NL + lane * EPL;
+  float* planes = (TRWP ? img_gm : a.gnext + size_t(b) * R * NL) + lane * EPL;
+  const uint8_t* pimg = a.p + size_t(b) * g.K_cap * g.E * L;
+  const uint8_t* qimg = a.q + size_t(b) * g.K_cap * g.E;
   const int l0 = lane * EPL;
   const int nvalid = FULL ? EPL : min(EPL, max(0, L - l0));
   const bool wpl = a.pot.w_planes != nullptr, rpl = TRWP && a.pot.rho_planes != nullptr;
@@ -93,14 +99,29 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   float* gvacc = a.gvacc + ((size_t(b) * kVRep + warp_global % kVRep) * 2 + (r & 1)) * L * L;
   const bool do_w = a.gw != nullptr;
   float* gwrow = do_w ? a.gw + (size_t(b) * (R / 2) + fam) * N : nullptr;
-  // plane offsets at a node, ascending d: TRWP skips r, ISGMR skips {r, r^1}
-  size_t poff[RT ? (TRWP ? RT - 1 : RT - 2) : 15];
+  // V'(mu, l) = V[mu*vs_mu + l*vs_l]: V(mu,l) on even directions, V(l,mu) on odd
+  const int vs_mu = (r & 1) ? 1 : L, vs_l = (r & 1) ? L : 1;
+  const float* Vl = a.pot.V + lane * EPL * vs_l;  // lane's first label
+  float* gvl = gvacc + lane * EPL;
+  const bool band = a.desc->banded != 0;
+  const int Dband = a.desc->D;
+  const float* gband = a.desc->g;
+  const bool band2 = band && Dband <= 2;
+  const float gD = gband[Dband];
+  // far dV contributions: per label, a one-entry cache of the last far target
+  // (targets move slowly along a scanline), flushed with RED on change
+  int fkey[EPL];
+  float fval[EPL];
 #pragma unroll
-  for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr) {
+  for (int i = 0; i < EPL; ++i) fkey[i] = -1, fval[i] = 0.0f;
+  // plane offsets (elements) at node 0, ascending d: TRWP skips r, ISGMR skips {r, r^1}
+  int poff[NPMAX];
+#pragma unroll
+  for (int rr = 0; rr < NPMAX; ++rr) {
     const int d = TRWP ? (rr < r ? rr : rr + 1) : (rr < (r & ~1) ? rr : rr + 2);
-    poff[rr] = size_t(d) * NL + l0;
+    poff[rr] = d * NL;
   }
-  // near-diagonal V'(l + delta, l), delta = -1, 0, 1 (for dw), per direction parity
+  // near-diagonal V'(l + delta, l), delta = -1, 0, 1 (for dw)
   float vloc[EPL][3];
 #pragma unroll
   for (int i = 0; i < EPL; ++i)
@@ -108,7 +129,7 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
     for (int t = 0; t < 3; ++t) {
       const int l = l0 + i, mu = l + t - 1;
       const bool ok = do_w && l < L && mu >= 0 && mu < L;
-      vloc[i][t] = ok ? __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+      vloc[i][t] = ok ? __ldg(a.pot.V + mu * vs_mu + l * vs_l) : 0.0f;
     }
 
   float vacc[EPL][3];  // near-diagonal dV partials, (mu = l + delta, l)
@@ -121,35 +142,47 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
   for (int li = warp_global; li < a.nlines; li += gridDim.x * wpc) {
     const LineDesc ld = a.lines[li];
     const int nsteps = ld.length - 1;
-    const size_t pq_base = (size_t(b) * g.K_cap + a.k) * g.E + g.dir_offset[r] + ld.edge_base;
+    // in-image index of edge (k, r, e) for node position j: ebase + j - 1
+    const uint32_t ebase = uint32_t(a.k) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
+    const int o_first = ld.first * L;
 
     // step s (0-based) handles node position j = nsteps - s (reverse order)
     auto issue = [&](int s) {
       const int slot = s % kStages;
       const uint32_t base_s = ring_s + 4u * uint32_t(slot * stage_f);
       const int j = nsteps - s;
-      const int cur = ld.first + j * st, prev = cur - st;
+      const int ocur = o_first + j * stL, oprev = ocur - stL;
       if (FULL || nvalid > 0) {
-        const size_t pn = size_t(prev) * L;
-        cp_slice_t<EPL, FULL>(base_s + 4u * l0, gmr + size_t(cur) * L + l0, nvalid);
-        cp_slice_t<EPL, FULL>(base_s + 4u * (LS + l0), gub + pn + l0, nvalid);
+        cp_slice_t<EPL, FULL>(base_s + 4u * l0, gmr + ocur, nvalid);
+        cp_slice_t<EPL, FULL>(base_s + 4u * (LS + l0), gub + oprev, nvalid);
 #pragma unroll
-        for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr)
-          if (RT || rr < NP) cp_slice_t<EPL, FULL>(base_s + 4u * ((2 + rr) * LS + l0), planes_base + poff[rr] + pn, nvalid);
+        for (int rr = 0; rr < NPMAX; ++rr)
+          if (RT || rr < NP) cp_slice_t<EPL, FULL>(base_s + 4u * ((2 + rr) * LS + l0), planes + poff[rr] + oprev, nvalid);
       }
-      // p row: the aligned words covering bytes [flat*L, flat*L + L)
-      const size_t flat = pq_base + j - 1;
-      const size_t pb = flat * L;
-      const uint32_t* pw = reinterpret_cast<const uint32_t*>(a.p) + (pb >> 2);
-      const int nwords = int(((pb + L - 1) >> 2) - (pb >> 2)) + 1;
+      const uint32_t e = ebase + uint32_t(j - 1);
       const uint32_t pdst = base_s + 4u * (rowsF * LS);
-      for (int t = lane; t < nwords; t += 32) cp_async_u32(pdst + 4u * t, pw + t, 4);
+      if (FULL) {
+        // row start e*L is 4-byte aligned; L/4 = 8*EPL words, at most 2 per lane
+        const uint32_t* pw = reinterpret_cast<const uint32_t*>(pimg + size_t(e) * L);
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (lane + 32 * t < 8 * EPL) cp_async_u32(pdst + 4u * (lane + 32 * t), pw + lane + 32 * t, 4);
+      } else {
+        // the aligned words covering bytes [e*L, e*L + L)
+        const size_t pb = size_t(e) * L;
+        const uint32_t* pw = reinterpret_cast<const uint32_t*>(pimg) + (pb >> 2);
+        const int nwords = int(((pb + L - 1) >> 2) - (pb >> 2)) + 1;
+        for (int t = lane; t < nwords; t += 32) cp_async_u32(pdst + 4u * t, pw + t, 4);
+      }
       // per-lane copies of the q word, w and rho (no cross-lane dependency)
       const uint32_t xdst = pdst + 4u * (8 * EPL + 4);
-      cp_async_u32(xdst + 4u * lane, reinterpret_cast<const uint32_t*>(a.q) + (flat >> 2), 4);
-      const int wnode = (r & 1) ? cur : prev;
-      if (wpl) cp_async_u32(xdst + 4u * (32 + lane), wrow + wnode, 4);
-      if (rpl) cp_async_u32(xdst + 4u * (64 + lane), rrow + wnode, 4);
+      cp_async_u32(xdst + 4u * lane, reinterpret_cast<const uint32_t*>(qimg) + (e >> 2), 4);
+      if (wpl || rpl) {
+        const int node = ld.first + j * st;
+        const int wnode = (r & 1) ? node : node - st;
+        if (wpl) cp_async_u32(xdst + 4u * (32 + lane), wrow + wnode, 4);
+        if (rpl) cp_async_u32(xdst + 4u * (64 + lane), rrow + wnode, 4);
+      }
     };
     // deferred per-edge dw: reduce parked lane partials of steps [s0, s0+cnt)
     auto flush_w = [&](int s0, int cnt) {
@@ -158,9 +191,8 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
         float t = 0.0f;
 #pragma unroll 8
         for (int c = 0; c < 32; ++c) t = fadd(t, s_wp[lane * 33 + c]);
-        const int j = nsteps - (s0 + lane);
-        const int cur = ld.first + j * st;
-        float* dst = gwrow + ((r & 1) ? cur : cur - st);
+        const int node = ld.first + (nsteps - (s0 + lane)) * st;
+        float* dst = gwrow + ((r & 1) ? node : node - st);
         *dst = fadd(*dst, t);
       }
       __syncwarp();
@@ -182,17 +214,22 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       __syncwarp();  // p words were copied by other lanes
       const float* slot = ring + (s % kStages) * stage_f;
       const int j = nsteps - s;
-      const int cur = ld.first + j * st, prev = cur - st;
-      const size_t flat = pq_base + j - 1;
-      const uint8_t* prow = reinterpret_cast<const uint8_t*>(slot + rowsF * LS) + ((flat * L) & 3) + l0;
+      const int ocur = o_first + j * stL, oprev = ocur - stL;
+      const uint32_t e = ebase + uint32_t(j - 1);
+      const uint8_t* prow = reinterpret_cast<const uint8_t*>(slot + rowsF * LS) + (FULL ? 0 : ((size_t(e) * L) & 3)) + l0;
       const float* xs = slot + rowsF * LS + 8 * EPL + 4;
-      const int qv = (__float_as_uint(xs[lane]) >> (8 * (flat & 3))) & 0xff;
+      const int qv = (__float_as_uint(xs[lane]) >> (8 * (e & 3))) & 0xff;
       const float w = wpl ? xs[32 + lane] : a.pot.w;
       const float rho = TRWP ? (rpl ? xs[64 + lane] : a.pot.rho) : 1.0f;
 
-      // ---- row = gm^r[cur] + carry; consume (zero) gm^r[cur]; reparam backward
+      // ---- row = gm^r[cur] + carry; consume (zero) gm^r[cur]
+      // The reparametrisation backward row[q] -= sum(row) (:48-53) only moves
+      // one entry, and the scatter is linear, so the scatter runs on the raw
+      // row while the warp sum is in flight; -sum is then added to the target
+      // of q (and g_q is corrected for dw / dV).
       float row[EPL];
-      int pm[EPL];
+      int d[EPL], mu[EPL];
+      float S;
       {
         float t[EPL];
         lds_slice<EPL>(t, slot + l0);
@@ -201,96 +238,123 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
         for (int i = 0; i < EPL; ++i) {
           row[i] = (FULL || i < nvalid) ? fadd(t[i], carry[i]) : 0.0f;
           lsum = fadd(lsum, row[i]);
-          pm[i] = (FULL || i < nvalid) ? int(prow[i]) : 0;
+          mu[i] = (FULL || i < nvalid) ? int(prow[i]) : l0 + i;
+          d[i] = mu[i] - (l0 + i);
         }
-        stg_slice<EPL>(gmr + size_t(cur) * L, l0, zero, nvalid, L);
-        const float S = warp_sum_f(lsum);
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) row[i] = l0 + i == qv ? fsub(row[i], S) : row[i];
+        stg_slice<EPL>(gmr - l0 + ocur, l0, zero, nvalid, L);
+        S = warp_sum_f(lsum);
       }
-      bool live[EPL];
-      int dl[EPL];
+      // split by target offset d = p[l] - l (masked copies are exact zeros
+      // elsewhere, so adding them unconditionally leaves every sum unchanged)
+      float gm1[EPL], g00[EPL], gp1[EPL];
+      bool far[EPL];
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        live[i] = (FULL || i < nvalid) && row[i] != 0.0f;
-        dl[i] = pm[i] - (l0 + i);
+        gm1[i] = d[i] == -1 ? row[i] : 0.0f;
+        g00[i] = d[i] == 0 ? row[i] : 0.0f;
+        gp1[i] = d[i] == 1 ? row[i] : 0.0f;
+        far[i] = uint32_t(d[i] + 1) > 2u;
       }
       // far targets' V' values, issued early so their latency overlaps the scatter
       float vfar[EPL];
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        const int l = l0 + i, mu = pm[i];
-        const bool far = do_w && live[i] && (dl[i] < -1 || dl[i] > 1);
-        vfar[i] = far ? __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+        if (band2) {
+          vfar[i] = gD;  // banded with D <= 2: every far candidate costs g(D)
+        } else {
+          const float* src = band ? gband + min(abs(d[i]), Dband) : Vl + mu[i] * vs_mu + i * vs_l;
+          vfar[i] = (do_w && far[i]) ? __ldg(src) : 0.0f;
+        }
       }
 
       // ---- scatter: acc[mu] = sum over l with p[l] = mu of g_l
       float acc[EPL];
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) acc[i] = 0.0f;
       if (EPL == 1) {
-        const float g0 = live[0] ? row[0] : 0.0f;
+        acc[0] = 0.0f;
+        const float g0 = row[0];
 #pragma unroll 8
         for (int lam = 0; lam < L; ++lam) {
-          const int pl = __shfl_sync(0xffffffffu, pm[0], lam);
+          const int pl = __shfl_sync(0xffffffffu, mu[0], lam);
           const float gl = __shfl_sync(0xffffffffu, g0, lam);
           acc[0] = (pl == lane && gl != 0.0f) ? fadd(acc[0], gl) : acc[0];
         }
       } else {
-        bool rem[EPL];
-        float accL = 0.0f, accR = 0.0f;
+        // acc[mu] gets g(mu) [d=0], g(mu+1) [d=-1], g(mu-1) [d=+1]; the labels
+        // just outside the lane's slice come from the neighbour lanes
+        float m1n = __shfl_down_sync(0xffffffffu, gm1[0], 1);
+        float p1n = __shfl_up_sync(0xffffffffu, gp1[EPL - 1], 1);
+        m1n = lane < 31 ? m1n : 0.0f;
+        p1n = lane > 0 ? p1n : 0.0f;
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
-          const float gi = row[i];
-          acc[i] = live[i] && dl[i] == 0 ? fadd(acc[i], gi) : acc[i];
-          if (i > 0) {
-            acc[i > 0 ? i - 1 : 0] = live[i] && dl[i] == -1 ? fadd(acc[i > 0 ? i - 1 : 0], gi) : acc[i > 0 ? i - 1 : 0];
-          } else {
-            accL = live[i] && dl[i] == -1 ? fadd(accL, gi) : accL;
-          }
-          if (i + 1 < EPL) {
-            acc[i + 1 < EPL ? i + 1 : 0] =
-                live[i] && dl[i] == 1 ? fadd(acc[i + 1 < EPL ? i + 1 : 0], gi) : acc[i + 1 < EPL ? i + 1 : 0];
-          } else {
-            accR = live[i] && dl[i] == 1 ? fadd(accR, gi) : accR;
-          }
-          rem[i] = live[i] && (dl[i] < -1 || dl[i] > 1);
+          const float m1 = i + 1 < EPL ? gm1[i + 1 < EPL ? i + 1 : 0] : m1n;
+          const float p1 = i > 0 ? gp1[i > 0 ? i - 1 : 0] : p1n;
+          acc[i] = fadd(fadd(g00[i], m1), p1);
         }
-        const float fromR = __shfl_down_sync(0xffffffffu, accL, 1);
-        const float fromL = __shfl_up_sync(0xffffffffu, accR, 1);
-        acc[EPL - 1] = lane < 31 ? fadd(acc[EPL - 1], fromR) : acc[EPL - 1];
-        acc[0] = lane > 0 ? fadd(acc[0], fromL) : acc[0];
-        // remaining targets: per round, the smallest and the largest pending
-        // target are summed with two independent warp reductions
-        while (true) {
-          uint32_t mn = 0xffffffffu, mx = 0u;
+        // far targets: per round, the smallest and the largest pending target
+        // are summed with two independent warp reductions (usually one round)
+        int klo[EPL], khi[EPL];
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) {
-            mn = rem[i] ? min(mn, uint32_t(pm[i])) : mn;
-            mx = rem[i] ? max(mx, uint32_t(pm[i]) + 1u) : mx;
-          }
-          const uint32_t kmin = __reduce_min_sync(0xffffffffu, mn);
-          if (kmin == 0xffffffffu) break;
-          const uint32_t kmax = __reduce_max_sync(0xffffffffu, mx) - 1u;
+        for (int i = 0; i < EPL; ++i) {
+          klo[i] = far[i] ? mu[i] : 0x7fffffff;
+          khi[i] = far[i] ? mu[i] : -1;
+        }
+        while (true) {
+          int mn = klo[0], mx = khi[0];
+#pragma unroll
+          for (int i = 1; i < EPL; ++i) mn = min(mn, klo[i]), mx = max(mx, khi[i]);
+          const int kmin = __reduce_min_sync(0xffffffffu, mn);
+          if (kmin == 0x7fffffff) break;
+          const int kmax = __reduce_max_sync(0xffffffffu, mx);
           float pa = 0.0f, pb2 = 0.0f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
-            const bool ia = rem[i] && uint32_t(pm[i]) == kmin;
-            const bool ib = rem[i] && uint32_t(pm[i]) == kmax && kmax != kmin;
-            pa = ia ? fadd(pa, row[i]) : pa;
-            pb2 = ib ? fadd(pb2, row[i]) : pb2;
-            rem[i] = rem[i] && !ia && !ib;
+            pa = fadd(pa, klo[i] == kmin ? row[i] : 0.0f);
+            pb2 = fadd(pb2, khi[i] == kmax ? row[i] : 0.0f);
           }
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) {
+            const bool done = klo[i] == kmin || khi[i] == kmax;
+            klo[i] = done ? 0x7fffffff : klo[i];
+            khi[i] = done ? -1 : khi[i];
+          }
+          if (kmax == kmin) pb2 = 0.0f;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) {
             pa = fadd(pa, __shfl_xor_sync(0xffffffffu, pa, o));
             pb2 = fadd(pb2, __shfl_xor_sync(0xffffffffu, pb2, o));
           }
+          const int ia = kmin - l0, ib = kmax - l0;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
-            acc[i] = int(kmin) == l0 + i ? fadd(acc[i], pa) : acc[i];
-            acc[i] = (kmax != kmin && int(kmax) == l0 + i) ? fadd(acc[i], pb2) : acc[i];
+            if (ia == i) acc[i] = fadd(acc[i], pa);
+            if (ib == i) acc[i] = fadd(acc[i], pb2);
           }
+        }
+      }
+      // reparametrisation backward: g_q = row_q - S lands on target p[q]
+      {
+        const int iq = qv - l0;
+        int muq = 0;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          if (iq == i) {
+            muq = mu[i];
+            row[i] = fsub(row[i], S);
+          }
+        }
+        muq = __shfl_sync(0xffffffffu, muq, qv / EPL);
+        const int im = muq - l0;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i)
+          if (im == i) acc[i] = fsub(acc[i], S);
+        // masks for dV / dw see the corrected g_q (only element iq changes)
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          if (iq != i) continue;
+          gm1[i] = d[i] == -1 ? row[i] : 0.0f;
+          g00[i] = d[i] == 0 ? row[i] : 0.0f;
+          gp1[i] = d[i] == 1 ? row[i] : 0.0f;
         }
       }
 
@@ -298,16 +362,16 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       {
         float outv[EPL], t[EPL], add[EPL];
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) add[i] = TRWP ? fmul(rho, acc[i]) : acc[i];
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) carry[i] = add[i];
-        const size_t pn = size_t(prev) * L;
+        for (int i = 0; i < EPL; ++i) {
+          add[i] = TRWP ? fmul(rho, acc[i]) : acc[i];
+          carry[i] = add[i];
+        }
         lds_slice<EPL>(t, slot + LS + l0);
 #pragma unroll
         for (int i = 0; i < EPL; ++i) outv[i] = fadd(t[i], add[i]);
-        stg_slice<EPL>(gub + pn, l0, outv, nvalid, L);
+        stg_slice<EPL>(gub - l0 + oprev, l0, outv, nvalid, L);
 #pragma unroll
-        for (int rr = 0; rr < (RT ? (TRWP ? RT - 1 : RT - 2) : 15); ++rr) {
+        for (int rr = 0; rr < NPMAX; ++rr) {
           if (RT || rr < NP) {
             const bool is_opp = TRWP && (rr < r ? rr : rr + 1) == opp;
             lds_slice<EPL>(t, slot + (2 + rr) * LS + l0);
@@ -316,7 +380,7 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
               const float v = fadd(t[i], add[i]);
               outv[i] = is_opp ? fsub(v, acc[i]) : v;
             }
-            stg_slice<EPL>(planes_base + poff[rr] - l0 + pn, l0, outv, nvalid, L);
+            stg_slice<EPL>(planes - l0 + poff[rr] + oprev, l0, outv, nvalid, L);
           }
         }
       }
@@ -325,15 +389,24 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
       float wpart = 0.0f;
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
-        const float gi = row[i];
-        const int d = dl[i];
-        const float vv = d == -1 ? vloc[i][0] : d == 0 ? vloc[i][1] : d == 1 ? vloc[i][2] : vfar[i];
-        wpart = live[i] ? fadd(wpart, fmul(gi, vv)) : wpart;
-        const float gwv = fmul(gi, w);
-        vacc[i][0] = live[i] && d == -1 ? fadd(vacc[i][0], gwv) : vacc[i][0];
-        vacc[i][1] = live[i] && d == 0 ? fadd(vacc[i][1], gwv) : vacc[i][1];
-        vacc[i][2] = live[i] && d == 1 ? fadd(vacc[i][2], gwv) : vacc[i][2];
-        if (live[i] && (d < -1 || d > 1)) atomicAdd(gvacc + size_t(pm[i]) * L + l0 + i, gwv);
+        if (do_w) {
+          const float vv = d[i] == -1 ? vloc[i][0] : d[i] == 0 ? vloc[i][1] : d[i] == 1 ? vloc[i][2] : vfar[i];
+          const float c = fmul(row[i], vv);
+          wpart = row[i] != 0.0f ? fadd(wpart, c) : wpart;
+        }
+        vacc[i][0] = fadd(vacc[i][0], fmul(gm1[i], w));
+        vacc[i][1] = fadd(vacc[i][1], fmul(g00[i], w));
+        vacc[i][2] = fadd(vacc[i][2], fmul(gp1[i], w));
+        if (far[i] && row[i] != 0.0f) {
+          const float gwv = fmul(row[i], w);
+          if (mu[i] == fkey[i]) {
+            fval[i] = fadd(fval[i], gwv);
+          } else {
+            if (fkey[i] >= 0) red_add_global(gvl + fkey[i] * L + i, fval[i]);
+            fkey[i] = mu[i];
+            fval[i] = gwv;
+          }
+        }
       }
       if (do_w) {
         s_wp[(s & 31) * 33 + lane] = wpart;
@@ -343,18 +416,21 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(BwdArgs a) {
     }
     // head row of plane r: its incoming scatter (carry) is dropped and the row
     // cleared, like the reference's plane clear / buffer swap (:122-123, :190-193)
-    stg_slice<EPL>(gmr + size_t(ld.first) * L, l0, zero, nvalid, L);
+    stg_slice<EPL>(gmr - l0 + o_first, l0, zero, nvalid, L);
     cp_wait<0>();
     __syncwarp();
   }
-  // flush near-diagonal dV partials
+  // flush the far-target caches and the near-diagonal dV partials
+#pragma unroll
+  for (int i = 0; i < EPL; ++i)
+    if (fkey[i] >= 0) red_add_global(gvl + fkey[i] * L + i, fval[i]);
 #pragma unroll
   for (int i = 0; i < EPL; ++i) {
     const int l = l0 + i;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const int mu = l + t - 1;
-      if (l < L && mu >= 0 && mu < L && vacc[i][t] != 0.0f) atomicAdd(gvacc + size_t(mu) * L + l, vacc[i][t]);
+      if (l < L && mu >= 0 && mu < L && vacc[i][t] != 0.0f) red_add_global(gvacc + mu * L + l, vacc[i][t]);
     }
   }
 }

@@ -10,7 +10,7 @@ static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
   const int wpc = warps_per_cta(a.nlines);
   const int smem = band2_smem_floats(EPL, rows) * int(sizeof(float)) * wpc;
   auto kern = fwd_band2_kernel<EPL, false, R, FULL>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
   kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);

@@ -21,6 +21,10 @@ inline int epl_for(int L) {
 // warps per CTA: few long chains -> spread them over every SM
 inline int warps_per_cta(int nlines) { return nlines >= 148 * 8 ? 4 : (nlines >= 148 * 2 ? 2 : 1); }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size) instead of on every launch (it costs host time on the launch path).
+cudaError_t ensure_dynamic_smem(const void* kern, int bytes);
+
 cudaError_t launch_fwd_generic(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 cudaError_t launch_fwd_band2_isgmr(const FwdArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_fwd_band2_trwp(const FwdArgs& a, int batch, cudaStream_t s);

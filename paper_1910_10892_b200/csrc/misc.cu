@@ -3,7 +3,30 @@
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
+
+#include "launch.hpp"
+
+namespace mrf {
+
+cudaError_t ensure_dynamic_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[{kern, dev}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
+}  // namespace mrf
 
 #include "../../include/mrf_cuda.h"
 #include "common.cuh"

@@ -314,6 +314,8 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   const size_t mb = messages_bytes(topo, pr), vb = gvacc_bytes(pr);
   const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb);
   if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
+  if (int64_t(R) * N * L >= (int64_t(1) << 31) || int64_t(K) * topo->host.total_edges() * L >= (int64_t(1) << 32))
+    fail(MRF_EINVAL, "backward: image too large (R*N*L must be < 2^31 and K*E*L < 2^32)");
   char* w = static_cast<char*>(ws);
   float* gm = reinterpret_cast<float*>(w);
   float* gnext = TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb));
@@ -337,11 +339,12 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   const Geometry g = make_geometry(topo, pr, K);
   const Potentials pot = make_potentials(pr);
   const LineDesc* lines = topo->device_lines();
+  PairDescHolder desc(pr, R, stream);
   for (int k = K - 1; k >= 0; --k) {
     for (int ri = 0; ri < R; ++ri) {
       const int r = TRWP ? R - 1 - ri : ri;  // TRWP replays directions in reverse (autodiff.hpp:147)
       BwdArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), r, p, q, k,
-                gm, gnext, grads->unary, grads->weight_planes, gvacc};
+                gm, gnext, grads->unary, grads->weight_planes, gvacc, desc.get()};
       // plane r of gm is consumed and left zero by the sweep (the reference's
       // plane clear, autodiff.hpp:190-193, and swap-and-clear, :122-123)
       launch_backward_sweep<TRWP>(a, B, stream);
