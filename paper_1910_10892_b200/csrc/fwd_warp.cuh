@@ -36,22 +36,18 @@ struct PairDesc {
 };
 
 // One block. Bit-level checks: symmetric Toeplitz, constant tail, and no -0
-// in the weight / rho planes (so no candidate value can be -0, which makes the
-// scanned minimum value equal to the first argmin's raw value).
-static __global__ void analyze_pairwise_kernel(const float* __restrict__ V, int L, const float* __restrict__ wplanes,
-                                        int64_t nw, float wconst, const float* __restrict__ rplanes, int64_t nr,
-                                        PairDesc* __restrict__ out) {
+// in the constant weight (planes are checked by scan_neg_zero_kernel), so no
+// candidate value can be -0, which makes the scanned minimum value equal to
+// the first argmin's raw value.
+static __global__ void analyze_pairwise_kernel(const float* __restrict__ V, int L, float wconst, int has_wplanes,
+                                               PairDesc* __restrict__ out) {
   int ok = 1;
   for (int i = threadIdx.x; i < L * L; i += blockDim.x) {
     const int a = i / L, b = i - a * L;
     const int d = a > b ? a - b : b - a;
     if (__float_as_uint(V[i]) != __float_as_uint(V[d])) ok = 0;
   }
-  for (int64_t i = threadIdx.x; i < nw; i += blockDim.x)
-    if (__float_as_uint(wplanes[i]) == 0x80000000u) ok = 0;
-  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x)
-    if (__float_as_uint(rplanes[i]) == 0x80000000u) ok = 0;
-  if (wplanes == nullptr && __float_as_uint(wconst) == 0x80000000u) ok = 0;
+  if (!has_wplanes && __float_as_uint(wconst) == 0x80000000u) ok = 0;
   ok = __syncthreads_and(ok);
   for (int d = threadIdx.x; d < 256; d += blockDim.x) out->g[d] = d < L ? V[d] : 0.0f;
   if (threadIdx.x == 0) {
@@ -61,6 +57,15 @@ static __global__ void analyze_pairwise_kernel(const float* __restrict__ V, int 
     out->D = D;
     out->banded = ok && (2 * D - 1) * 2 <= L;
   }
+}
+
+// Runs after analyze_pairwise_kernel: any -0 in the weight / rho planes
+// disables the banded strategy (grid-wide scan; every writer writes 0).
+static __global__ void scan_neg_zero_kernel(const uint32_t* __restrict__ x, int64_t n, PairDesc* __restrict__ out) {
+  int found = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    found |= __ldg(x + i) == 0x80000000u;
+  if (__syncthreads_or(found) && threadIdx.x == 0) out->banded = 0;
 }
 
 struct FwdArgs {

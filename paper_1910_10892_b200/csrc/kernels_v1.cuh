@@ -286,4 +286,19 @@ __global__ void broadcast_planes_kernel(int B, int R, int64_t NL, const float* _
   dst[i] = src[b * NL + rem % NL];
 }
 
+// make_gradients + gm init (autodiff.hpp:33-44, :72-74) in one pass:
+// gu[b] = dc[b] and gm[b][r] = dc[b] for every r. float4 body (NL % 4 == 0),
+// grid-stride over (image, chunk); one read of dc, R+1 writes.
+__global__ void init_grads_kernel(int B, int R, int64_t NL4, const float4* __restrict__ gc, float4* __restrict__ gu,
+                                  float4* __restrict__ gm) {
+  const int64_t total = int64_t(B) * NL4;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t b = i / NL4, x = i - b * NL4;
+    const float4 v = __ldcs(gc + i);
+    __stcs(gu + i, v);
+    float4* dst = gm + b * R * NL4 + x;
+    for (int r = 0; r < R; ++r) __stcs(dst + r * NL4, v);
+  }
+}
+
 }  // namespace mrf

@@ -235,10 +235,14 @@ class PairDescHolder {
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_), sizeof(PairDesc), s), "cudaMallocAsync(desc)");
     const int64_t planes = int64_t(pr->batch) * (R / 2) * pr->height * pr->width;
     ProfScope ps(s, MRF_KCLASS_AUX);
-    analyze_pairwise_kernel<<<1, 256, 0, s>>>(pr->pairwise, pr->labels, pr->weight_planes,
-                                              pr->weight_planes ? planes : 0, pr->weight, pr->rho_planes,
-                                              pr->rho_planes ? planes : 0, d_);
+    analyze_pairwise_kernel<<<1, 256, 0, s>>>(pr->pairwise, pr->labels, pr->weight, pr->weight_planes != nullptr, d_);
     cuda_check(cudaGetLastError(), "analyze_pairwise launch");
+    for (const float* pl : {pr->weight_planes, pr->rho_planes}) {
+      if (!pl) continue;
+      const int blocks = int(std::min<int64_t>(148 * 4, (planes + 255) / 256));
+      scan_neg_zero_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(pl), planes, d_);
+      cuda_check(cudaGetLastError(), "scan_neg_zero launch");
+    }
   }
   ~PairDescHolder() { cudaFreeAsync(d_, s_); }
   const PairDesc* get() const { return d_; }
@@ -323,16 +327,25 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   const size_t NL = size_t(N) * L;
 
   // make_gradients (autodiff.hpp:33-44) and gm <- dc for every r (:72-74)
-  cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
-             "copy grad_cost");
   if (grads->weight_planes)
     cuda_check(cudaMemsetAsync(grads->weight_planes, 0, sizeof(float) * B * (R / 2) * N, stream), "zero dw");
   cuda_check(cudaMemsetAsync(gvacc, 0, vb, stream), "zero dV accumulators");
   {
-    const int64_t total = int64_t(B) * R * NL;
     ProfScope ps(stream, MRF_KCLASS_AUX);
-    broadcast_planes_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, R, int64_t(NL), grad_cost, gm);
-    cuda_check(cudaGetLastError(), "broadcast launch");
+    const bool vec = (NL % 4) == 0 && (reinterpret_cast<uintptr_t>(grad_cost) % 16) == 0 &&
+                     (reinterpret_cast<uintptr_t>(grads->unary) % 16) == 0;
+    if (vec) {
+      init_grads_kernel<<<148 * 8, 256, 0, stream>>>(B, R, int64_t(NL / 4), reinterpret_cast<const float4*>(grad_cost),
+                                                     reinterpret_cast<float4*>(grads->unary),
+                                                     reinterpret_cast<float4*>(gm));
+      cuda_check(cudaGetLastError(), "init_grads launch");
+    } else {
+      cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
+                 "copy grad_cost");
+      const int64_t total = int64_t(B) * R * NL;
+      broadcast_planes_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, R, int64_t(NL), grad_cost, gm);
+      cuda_check(cudaGetLastError(), "broadcast launch");
+    }
   }
   if (!TRWP) cuda_check(cudaMemsetAsync(gnext, 0, mb, stream), "zero gm_next");
 
