@@ -14,7 +14,7 @@
 namespace mrf {
 
 __host__ __device__ constexpr int band2_smem_floats(int EPL, int rows) {
-  return ((kStages * rows) * 32 * EPL + kStages * 64 + 31) / 32 * 32;
+  return ((kStages * rows + 1) * 32 * EPL + kStages * 64 + 31) / 32 * 32;
 }
 
 // EPL bytes (one per label) -> one (or a few) packed stores at row + l0.
@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   float* ring = smem + size_t(wid) * band2_smem_floats(EPL, ROWS);
   float* s_x = ring + kStages * ROWS * LS;
+  float* s_u = s_x + kStages * 64;  // far-candidate costs of the current node
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   const uint32_t x_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_x));
 
@@ -149,6 +150,13 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
         for (int i = 0; i < EPL; ++i) base[i] = i < nvalid ? base[i] : kInf;
       }
 
+      // left / right far winners per label, two exact strategies:
+      //  * EPL >= 4: warp prefix / suffix (value, first index) scans of u
+      //    (few shuffle rounds per label, best when a lane owns many labels);
+      //  * EPL <= 2: reductions around the global first argmin (below).
+      float LV[EPL], RV[EPL], bl, br;
+      int LI[EPL], RI[EPL];
+      if constexpr (EPL >= 4) {
       // ---- far-candidate cost, prefix / suffix (value, first index) scans
       float u[EPL], pv[EPL], sv[EPL];
       int pi[EPL], si[EPL];
@@ -205,8 +213,8 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
 
       // ---- neighbours across lanes: base(l0-1), base(l0+EPL), far segment
       // summaries at l-2 / l+2 for the lane's first / last two labels
-      float bl = __shfl_up_sync(0xffffffffu, base[EPL - 1], 1);
-      float br = __shfl_down_sync(0xffffffffu, base[0], 1);
+      bl = __shfl_up_sync(0xffffffffu, base[EPL - 1], 1);
+      br = __shfl_down_sync(0xffffffffu, base[0], 1);
       bl = lane > 0 ? bl : kInf;
       br = lane < 31 ? br : kInf;
       constexpr int E2 = EPL >= 2 ? 2 : 1;  // labels per lane needing the neighbour's far summary
@@ -225,19 +233,112 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
         svp[e] = lane + SH < 32 ? svp[e] : kInf;
       }
 
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        LV[i] = i >= 2 ? pv[i >= 2 ? i - 2 : 0] : pvm[i < E2 ? i : 0];
+        LI[i] = i >= 2 ? pi[i >= 2 ? i - 2 : 0] : pim[i < E2 ? i : 0];
+        const int hi = i + 2 - EPL;  // >= 0: right far summary lives in lane + SH
+        RV[i] = hi < 0 ? sv[hi < 0 ? i + 2 : 0] : svp[hi >= 0 && hi < E2 ? hi : 0];
+        RI[i] = hi < 0 ? si[hi < 0 ? i + 2 : 0] : sip[hi >= 0 && hi < E2 ? hi : 0];
+      }
+      } else {
+      // ---- far candidates: u(mu) = fl(base(mu) + fl(w g(2))). With mu* the
+      // global first argmin of u, every label l with |l - mu*| >= 2 has mu* in
+      // its far set and no earlier index reaches u(mu*), so its far winner is
+      // (u*, mu*) -- in the left segment when mu* < l (first in index order,
+      // wins ties; the right segment can then never hold the first argmin)
+      // or in the right one when mu* > l (the left can then never reach u*).
+      // Only l in {mu*-1, mu*, mu*+1} need the prefix winners over [0, mu*-3],
+      // [0, mu*-2], [0, mu*-1] and the suffix winners over [mu*+1, L),
+      // [mu*+2, L), [mu*+3, L): two masked warp reductions plus four values.
+      float u[EPL];
+      uint32_t ku[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        u[i] = fadd(base[i], c);  // +inf on invalid labels (base +inf)
+        ku[i] = order_key(u[i]);
+        s_u[l0 + i] = u[i];
+      }
+      uint32_t mk = ku[0];
+      int mi = l0;
+#pragma unroll
+      for (int i = 1; i < EPL; ++i) {
+        const bool t = ku[i] < mk;
+        mk = t ? ku[i] : mk;
+        mi = t ? l0 + i : mi;
+      }
+      const uint32_t gk = __reduce_min_sync(0xffffffffu, mk);
+      const int mstar = __reduce_min_sync(0xffffffffu, mk == gk ? mi : 0x7fffffff);
+      const float ustar = key_value(gk);
+      uint32_t pk = 0xffffffffu, sk = 0xffffffffu;
+      int pix = 0x7fffffff, six = 0x7fffffff;
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int l = l0 + i;
+        const bool tp = l <= mstar - 3 && ku[i] < pk;
+        pk = tp ? ku[i] : pk;
+        pix = tp ? l : pix;
+        const bool ts = l >= mstar + 3 && ku[i] < sk;
+        sk = ts ? ku[i] : sk;
+        six = ts ? l : six;
+      }
+      const uint32_t pkm = __reduce_min_sync(0xffffffffu, pk);
+      const uint32_t skm = __reduce_min_sync(0xffffffffu, sk);
+      const int pim = __reduce_min_sync(0xffffffffu, pk == pkm ? pix : 0x7fffffff);
+      const int sim = __reduce_min_sync(0xffffffffu, sk == skm ? six : 0x7fffffff);
+      __syncwarp();
+      const float um2 = mstar >= 2 ? s_u[mstar - 2] : kInf, um1 = mstar >= 1 ? s_u[mstar - 1] : kInf;
+      const float up1 = mstar + 1 < L ? s_u[mstar + 1] : kInf, up2 = mstar + 2 < L ? s_u[mstar + 2] : kInf;
+      // prefix winners P3, P2, P1 and suffix winners S3, S2, S1 (empty = +inf)
+      const float P3v = pkm == 0xffffffffu ? kInf : key_value(pkm);
+      const int P3i = pim;
+      const bool t2 = um2 < P3v;
+      const float P2v = t2 ? um2 : P3v;
+      const int P2i = t2 ? mstar - 2 : P3i;
+      const bool t1 = um1 < P2v;
+      const float P1v = t1 ? um1 : P2v;
+      const int P1i = t1 ? mstar - 1 : P2i;
+      const float S3v = skm == 0xffffffffu ? kInf : key_value(skm);
+      const int S3i = sim;
+      const bool s2 = S3v < up2;  // earlier element wins ties
+      const float S2v = s2 ? S3v : up2;
+      const int S2i = s2 ? S3i : mstar + 2;
+      const bool s1 = S2v < up1;
+      const float S1v = s1 ? S2v : up1;
+      const int S1i = s1 ? S2i : mstar + 1;
+      __syncwarp();  // s_u reads done before the next node overwrites it
+
+      // ---- neighbours across lanes for the near band: base(l0-1), base(l0+EPL)
+      bl = __shfl_up_sync(0xffffffffu, base[EPL - 1], 1);
+      br = __shfl_down_sync(0xffffffffu, base[0], 1);
+      bl = lane > 0 ? bl : kInf;
+      br = lane < 31 ? br : kInf;
+
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) {
+        const int dl = l0 + i - mstar;
+        float lv = dl >= 2 ? ustar : kInf, rv = dl <= -2 ? ustar : kInf;
+        int lix = mstar, rix = mstar;
+        lv = dl == -1 ? P3v : lv, lix = dl == -1 ? P3i : lix;
+        lv = dl == 0 ? P2v : lv, lix = dl == 0 ? P2i : lix;
+        lv = dl == 1 ? P1v : lv, lix = dl == 1 ? P1i : lix;
+        rv = dl == -1 ? S1v : rv, rix = dl == -1 ? S1i : rix;
+        rv = dl == 0 ? S2v : rv, rix = dl == 0 ? S2i : rix;
+        rv = dl == 1 ? S3v : rv, rix = dl == 1 ? S3i : rix;
+        LV[i] = lv, LI[i] = lix, RV[i] = rv, RI[i] = rix;
+      }
+      }
+
       // ---- combine in index order: [0,l-2] | l-1 | l | l+1 | [l+2,L)
       float out[EPL];
       int am[EPL];
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         const int l = l0 + i;
-        const float lv = i >= 2 ? pv[i >= 2 ? i - 2 : 0] : pvm[i < E2 ? i : 0];
-        const int lix = i >= 2 ? pi[i >= 2 ? i - 2 : 0] : pim[i < E2 ? i : 0];
+        const float lv = LV[i], rv = RV[i];
+        const int lix = LI[i], rix = RI[i];
         const float bm1 = i >= 1 ? base[i >= 1 ? i - 1 : 0] : bl;
         const float bp1 = i + 1 < EPL ? base[i + 1 < EPL ? i + 1 : 0] : br;
-        const int hi = i + 2 - EPL;  // >= 0: right far summary lives in lane + SH
-        const float rv = hi < 0 ? sv[hi < 0 ? i + 2 : 0] : svp[hi >= 0 && hi < E2 ? hi : 0];
-        const int rix = hi < 0 ? si[hi < 0 ? i + 2 : 0] : sip[hi >= 0 && hi < E2 ? hi : 0];
         float best = lv;
         int arg = lv < kInf ? lix : 0;
         float v = fadd(bm1, wg1);

@@ -21,15 +21,19 @@ def full(rep, out, label=""):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     res = []
     for vals in rows[2:]:
         d = dict(zip(hdr, vals))
 
         def num(k):
             try:
-                return float(d.get(k, "nan").replace(",", ""))
+                v = float(d.get(k, "nan").replace(",", ""))
             except ValueError:
                 return None
+            return v * scale.get(units.get(k, ""), 1.0)
 
         stalls = {}
         for k in hdr:
