@@ -25,7 +25,7 @@ NVCC_FLAGS = ARCH + [
     # IEEE division/sqrt, no flush-to-zero (SURVEY.md §7 hard part 1).
     "-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true",
     "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-]
+] + os.environ.get("MRF_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:

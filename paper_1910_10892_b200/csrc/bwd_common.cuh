@@ -1,0 +1,143 @@
+// Backward over per-direction scatter planes (sm_100a): the algebra shared by
+// the backward kernels (bwd_split.cuh), isgmr_backward / trwp_backward
+// (autodiff.hpp:63-126, :133-197) restated so that a node step reads the
+// gradient it consumes and writes ONE row.
+//
+// The reference keeps message-gradient planes gm[d] and, for every label l of
+// every edge (prev -> cur) of direction r, adds the reparametrised row g_l to
+// dtheta[prev][p_l], gm[r][prev][p_l] (the sweep's own chain) and to the
+// other planes at prev (TRWP: rho*g to every d, -g extra to r^1; ISGMR: g to
+// gm_next[d] for d not in {r, r^1}). All those additions are the same
+// per-node vector acc_r[prev][mu] = sum_{l : p_l = mu} g_l (times rho). So
+// the sweep stores acc_r once, into plane A[r], and the planes the reference
+// accumulates are recovered when they are consumed:
+//
+//   TRWP  gm[r](cur) at sweep (k, r) =
+//           [k == K-1] dc(cur)                           (initial broadcast, :142-144)
+//         + sum_{d != r, in sweep order since plane r was last cleared}
+//               rho_d(cur) A[d](cur) - [d == r^1] A[d](cur)
+//         (A[d] holds direction d's most recent sweep: iteration k+1 for d < r,
+//          k for d > r; at k == K-1 only d > r have run; the clear of :190-193
+//          is the window boundary)
+//   ISGMR gm[r](cur) at iteration k = [k == K-1] dc(cur)
+//         + [k < K-1] sum_{d not in {r, r^1}} A_{k+1}[d](cur)   (gm_next, swap :122-123)
+//   dtheta = dc + sum_{k, d} rho_d A_k[d]  (accumulated once per iteration by
+//                                           dtheta_acc_kernel)
+//
+// plus, as in the reference, the sweep's own chain ("carry": rho_r acc_r at
+// prev is exactly what node prev reads next from gm[r]). Per node and sweep
+// that is R-1 (TRWP) / R-2 (ISGMR) row reads and one row write instead of
+// R+1 read-modify-writes, and ISGMR's directions become independent within an
+// iteration (one launch per iteration, all R directions' scanlines).
+// Per-mu aggregation and the regrouped row sums reorder the reference's
+// per-label additions, so gradients match within the 1e-5 tolerance rather
+// than bitwise. The tail row of every line is written as zeros (no edge has it as prev),
+// so planes never need clearing.
+#pragma once
+
+#include "common.cuh"
+#include "fwd_warp.cuh"
+
+namespace mrf {
+
+constexpr int kVRep = 4;  // dV accumulation replicas per image
+
+struct AccArgs {
+  Geometry g;
+  Potentials pot;
+  const LineDesc* lines;  // TRWP: direction r's lines; ISGMR: every direction's lines
+  int nlines;
+  const uint8_t* p;
+  const uint8_t* q;
+  int k;
+  const float* dc;   // [B][N][L] cost gradient (read at k == K-1)
+  const float* ain;  // [B][R][N][L] planes read (TRWP: == aout; ISGMR: iteration k+1)
+  float* aout;       // [B][R][N][L] planes written (plane r of each line)
+  float* gw;         // TRWP: [B][R/2][N] (family planes); ISGMR: [B][R][N] per direction; or null
+  float* gvacc;      // [B][kVRep][2][L][L]
+  const PairDesc* desc;
+};
+
+// row slots: TRWP R-1 planes (+ dc at k == K-1 needs at most R in total), ISGMR R-2 planes or dc
+__host__ __device__ constexpr int acc_rows(bool trwp, int R) { return trwp ? R : (R - 2 > 1 ? R - 2 : 1); }
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fadd(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// dtheta[n] += sum_d rho_d(n) A[d](n) (TRWP; rho_d(n) is the tree coefficient
+// of direction d's edge with n as prev) or sum_d A[d](n) (ISGMR), d
+// ascending: the iteration's contribution of every sweep to the unary
+// gradient (autodiff.hpp:101 / :173). Image b = blockIdx.y; float4 when L % 4
+// == 0 (a vector never straddles two nodes).
+template <bool TRWP>
+__global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__ A, float rho,
+                                  const float* __restrict__ rho_planes, Geometry g, float* __restrict__ dtheta) {
+  const int NL = N * L;
+  const int b = blockIdx.y;
+  const float* Ab = A + size_t(b) * R * NL;
+  float* dt = dtheta + size_t(b) * NL;
+  auto rho_of = [&](int d, int n) {
+    if (!TRWP) return 1.0f;
+    if (!rho_planes) return rho;
+    const int wn = (d & 1) ? n + g.node_step[d] : n;
+    return __ldg(rho_planes + (size_t(b) * (R / 2) + (d >> 1)) * N + min(max(wn, 0), N - 1));
+  };
+  if ((L & 3) == 0) {
+    const int n4 = NL >> 2;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+      const int n = (i << 2) / L;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int d = 0; d < R; ++d) {
+        float4 v = __ldcs(reinterpret_cast<const float4*>(Ab + size_t(d) * NL) + i);
+        if (TRWP) {
+          const float rd = rho_of(d, n);
+          v.x = fmul(rd, v.x), v.y = fmul(rd, v.y), v.z = fmul(rd, v.z), v.w = fmul(rd, v.w);
+        }
+        s.x = fadd(s.x, v.x), s.y = fadd(s.y, v.y), s.z = fadd(s.z, v.z), s.w = fadd(s.w, v.w);
+      }
+      float4 o = reinterpret_cast<float4*>(dt)[i];
+      o.x = fadd(o.x, s.x), o.y = fadd(o.y, s.y), o.z = fadd(o.z, s.z), o.w = fadd(o.w, s.w);
+      reinterpret_cast<float4*>(dt)[i] = o;
+    }
+  } else {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NL; i += gridDim.x * blockDim.x) {
+      const int n = i / L;
+      float s = 0.0f;
+      for (int d = 0; d < R; ++d) {
+        const float v = __ldcs(Ab + size_t(d) * NL + i);
+        s = fadd(s, TRWP ? fmul(rho_of(d, n), v) : v);
+      }
+      dt[i] = fadd(dt[i], s);
+    }
+  }
+}
+
+// ISGMR per-direction dw partials -> family planes: gw[b][f][n] = dwr[b][2f][n] + dwr[b][2f+1][n]
+static __global__ void combine_dw_kernel(int B, int R, int N, const float* __restrict__ dwr, float* __restrict__ gw) {
+  const int64_t total = int64_t(B) * (R / 2) * N;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t n = i % N, bf = i / N;
+    gw[i] = fadd(dwr[(2 * bf) * N + n], dwr[(2 * bf + 1) * N + n]);
+  }
+}
+
+// dV[b][x][y] = sum_rep acc[b][rep][0][x][y] + acc[b][rep][1][y][x]
+static __global__ void reduce_gvacc_kernel(int B, int L, const float* __restrict__ acc, float* __restrict__ gv) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t LL = int64_t(L) * L;
+  if (i >= B * LL) return;
+  const int b = int(i / LL);
+  const int xy = int(i - b * LL), x = xy / L, y = xy - x * L;
+  float s = 0.0f;
+  for (int rep = 0; rep < kVRep; ++rep) {
+    const float* base = acc + (size_t(b) * kVRep + rep) * 2 * LL;
+    s = fadd(s, base[xy]);
+    s = fadd(s, base[LL + size_t(y) * L + x]);
+  }
+  gv[i] = s;
+}
+
+}  // namespace mrf

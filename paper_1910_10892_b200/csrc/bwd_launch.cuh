@@ -1,0 +1,52 @@
+// Launcher for the warp-specialised backward (bwd_split.cuh): one CTA per
+// scanline (CHAIN + POST + kSplitPre producer warps).
+#pragma once
+
+#include "bwd_common.cuh"
+#include "bwd_split.cuh"
+#include "launch.hpp"
+
+namespace mrf {
+
+template <int EPL, bool TRWP, int RT, bool FULL, bool BAND>
+static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
+  constexpr int NPRE = kSplitPre;
+  const int smem = split_smem_floats(EPL, acc_rows(TRWP, a.g.R), NPRE) * int(sizeof(float));
+  auto kern = bwd_split_kernel<EPL, TRWP, RT, FULL, NPRE, BAND>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int blocks = a.nlines < 65535 ? a.nlines : 65535;
+  kern<<<dim3(blocks, batch), 32 * (2 + NPRE), smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+// The pairwise strategy is known on the device only: both variants are
+// launched and the one that does not own the sweep exits at once.
+template <int EPL, bool TRWP, int RT, bool FULL>
+static cudaError_t run_split(const AccArgs& a, int batch, cudaStream_t s) {
+  cudaError_t e = run_split1<EPL, TRWP, RT, FULL, true>(a, batch, s);
+  if (e != cudaSuccess) return e;
+  return run_split1<EPL, TRWP, RT, FULL, false>(a, batch, s);
+}
+
+template <int EPL, bool TRWP>
+static cudaError_t run_split_r(const AccArgs& a, int batch, cudaStream_t s) {
+  const bool full = a.g.L == 32 * EPL;
+  if (a.g.R == 4) return full ? run_split<EPL, TRWP, 4, true>(a, batch, s) : run_split<EPL, TRWP, 4, false>(a, batch, s);
+  if (a.g.R == 8) return full ? run_split<EPL, TRWP, 8, true>(a, batch, s) : run_split<EPL, TRWP, 8, false>(a, batch, s);
+  return run_split<EPL, TRWP, 0, false>(a, batch, s);
+}
+
+template <bool TRWP>
+static cudaError_t launch_bwd_sweep(const AccArgs& a, int batch, cudaStream_t s) {
+  if (a.nlines == 0) return cudaSuccess;
+  switch (epl_for(a.g.L)) {
+    case 1: return run_split_r<1, TRWP>(a, batch, s);
+    case 2: return run_split_r<2, TRWP>(a, batch, s);
+    case 4: return run_split_r<4, TRWP>(a, batch, s);
+    case 6: return run_split_r<6, TRWP>(a, batch, s);
+    default: return run_split_r<8, TRWP>(a, batch, s);
+  }
+}
+
+}  // namespace mrf

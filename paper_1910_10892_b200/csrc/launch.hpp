@@ -4,7 +4,7 @@
 
 #include <cuda_runtime.h>
 
-#include "bwd_warp.cuh"
+#include "bwd_common.cuh"
 #include "fwd_warp.cuh"
 
 namespace mrf {
@@ -28,8 +28,8 @@ cudaError_t ensure_dynamic_smem(const void* kern, int bytes);
 cudaError_t launch_fwd_generic(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 cudaError_t launch_fwd_band2_isgmr(const FwdArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_fwd_band2_trwp(const FwdArgs& a, int batch, cudaStream_t s);
-cudaError_t launch_bwd_isgmr(const BwdArgs& a, int batch, cudaStream_t s);
-cudaError_t launch_bwd_trwp(const BwdArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_bwd_isgmr(const AccArgs& a, int batch, cudaStream_t s);
+cudaError_t launch_bwd_trwp(const AccArgs& a, int batch, cudaStream_t s);
 
 
 }  // namespace mrf

@@ -125,8 +125,10 @@ struct mrf_topology_s {
   std::vector<size_t> dir_start;                   // offset of dir r's block in the upload
   std::vector<std::vector<LineDesc>> dir_lines_all;  // per direction incl. single-node lines (backward)
   std::vector<size_t> dir_all_start;
+  std::vector<LineDesc> every_line;                // ISGMR backward: every direction incl. single nodes, longest first
+  size_t every_start = 0;
   struct Dev {
-    LineDesc* lines = nullptr;  // [all_lines | dir 0 | ... | dir R-1 | all-lines dir 0 | ...]
+    LineDesc* lines = nullptr;  // [all_lines | dir 0 | ... | dir R-1 | all-lines dir 0 | ... | every_line]
   };
   std::map<int, Dev> dev;
   std::mutex mu;
@@ -155,7 +157,11 @@ struct mrf_topology_s {
     for (int r = 0; r < host.num_dirs(); ++r) {
       dir_all_start.push_back(off);
       off += dir_lines_all[r].size();
+      every_line.insert(every_line.end(), dir_lines_all[r].begin(), dir_lines_all[r].end());
     }
+    std::stable_sort(every_line.begin(), every_line.end(),
+                     [](const LineDesc& a, const LineDesc& b) { return a.length > b.length; });
+    every_start = off;
   }
 
   ~mrf_topology_s() {
@@ -177,6 +183,7 @@ struct mrf_topology_s {
     std::vector<LineDesc> all(all_lines);
     for (auto& v : dir_lines) all.insert(all.end(), v.begin(), v.end());
     for (auto& v : dir_lines_all) all.insert(all.end(), v.begin(), v.end());
+    all.insert(all.end(), every_line.begin(), every_line.end());
     Dev dv;
     cuda_check(cudaMalloc(&dv.lines, sizeof(LineDesc) * std::max<size_t>(1, all.size())), "cudaMalloc(lines)");
     cuda_check(cudaMemcpy(dv.lines, all.data(), sizeof(LineDesc) * all.size(), cudaMemcpyHostToDevice),
@@ -303,66 +310,71 @@ size_t gvacc_bytes(const mrf_problem_f32* pr) {
   return sizeof(float) * size_t(pr->batch) * kVRep * 2 * pr->labels * pr->labels;
 }
 
-template <bool TRWP>
-void launch_backward_sweep(const BwdArgs& a, int batch, cudaStream_t stream) {
-  if (a.nlines == 0) return;
-  ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
-  cuda_check(TRWP ? launch_bwd_trwp(a, batch, stream) : launch_bwd_isgmr(a, batch, stream), "bwd_warp_kernel launch");
-}
+size_t dwr_bytes(const mrf_problem_f32* pr, int R, int N) { return sizeof(float) * size_t(pr->batch) * R * N; }
 
+// Backward (autodiff.hpp:63-197) over per-direction scatter planes A
+// (bwd_common.cuh, bwd_split.cuh): TRWP replays directions R-1..0 per iteration, one launch
+// each (directions are sequential, :147); ISGMR's directions only read the
+// previous iteration's planes, so one launch covers all of them. After each
+// iteration the unary gradient collects every sweep's contribution.
 template <bool TRWP>
 void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const uint8_t* p, const uint8_t* q,
                   const float* grad_cost, const mrf_grads_f32* grads, void* ws, size_t ws_bytes,
                   cudaStream_t stream) {
   const int R = topo->host.num_dirs(), N = topo->host.nodes(), L = pr->labels, B = pr->batch;
   const size_t mb = messages_bytes(topo, pr), vb = gvacc_bytes(pr);
-  const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb);
+  const bool isgmr_dw = !TRWP && grads->weight_planes;
+  const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb) + (TRWP ? 0 : align_up(dwr_bytes(pr, R, N)));
   if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
   if (int64_t(R) * N * L >= (int64_t(1) << 31) || int64_t(K) * topo->host.total_edges() * L >= (int64_t(1) << 32))
     fail(MRF_EINVAL, "backward: image too large (R*N*L must be < 2^31 and K*E*L < 2^32)");
   char* w = static_cast<char*>(ws);
-  float* gm = reinterpret_cast<float*>(w);
-  float* gnext = TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb));
+  float* A[2] = {reinterpret_cast<float*>(w), TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb))};
   float* gvacc = reinterpret_cast<float*>(w + align_up(mb) * (TRWP ? 1 : 2));
+  float* dwr = TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb) * 2 + align_up(vb));
   const size_t NL = size_t(N) * L;
 
-  // make_gradients (autodiff.hpp:33-44) and gm <- dc for every r (:72-74)
+  // make_gradients (autodiff.hpp:33-44): dtheta <- dc, dV <- 0, dw <- 0
   if (grads->weight_planes)
     cuda_check(cudaMemsetAsync(grads->weight_planes, 0, sizeof(float) * B * (R / 2) * N, stream), "zero dw");
+  if (isgmr_dw) cuda_check(cudaMemsetAsync(dwr, 0, dwr_bytes(pr, R, N), stream), "zero dw partials");
   cuda_check(cudaMemsetAsync(gvacc, 0, vb, stream), "zero dV accumulators");
-  {
-    ProfScope ps(stream, MRF_KCLASS_AUX);
-    const bool vec = (NL % 4) == 0 && (reinterpret_cast<uintptr_t>(grad_cost) % 16) == 0 &&
-                     (reinterpret_cast<uintptr_t>(grads->unary) % 16) == 0;
-    if (vec) {
-      init_grads_kernel<<<148 * 8, 256, 0, stream>>>(B, R, int64_t(NL / 4), reinterpret_cast<const float4*>(grad_cost),
-                                                     reinterpret_cast<float4*>(grads->unary),
-                                                     reinterpret_cast<float4*>(gm));
-      cuda_check(cudaGetLastError(), "init_grads launch");
-    } else {
-      cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
-                 "copy grad_cost");
-      const int64_t total = int64_t(B) * R * NL;
-      broadcast_planes_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, R, int64_t(NL), grad_cost, gm);
-      cuda_check(cudaGetLastError(), "broadcast launch");
-    }
-  }
-  if (!TRWP) cuda_check(cudaMemsetAsync(gnext, 0, mb, stream), "zero gm_next");
+  cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
+             "copy grad_cost");
 
   const Geometry g = make_geometry(topo, pr, K);
   const Potentials pot = make_potentials(pr);
   const LineDesc* lines = topo->device_lines();
   PairDescHolder desc(pr, R, stream);
+  const dim3 dt_grid(unsigned(std::min<int64_t>(148 * 8 / B + 1, (int64_t(NL) / 4 + 255) / 256)), unsigned(B));
   for (int k = K - 1; k >= 0; --k) {
-    for (int ri = 0; ri < R; ++ri) {
-      const int r = TRWP ? R - 1 - ri : ri;  // TRWP replays directions in reverse (autodiff.hpp:147)
-      BwdArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), r, p, q, k,
-                gm, gnext, grads->unary, grads->weight_planes, gvacc, desc.get()};
-      // plane r of gm is consumed and left zero by the sweep (the reference's
-      // plane clear, autodiff.hpp:190-193, and swap-and-clear, :122-123)
-      launch_backward_sweep<TRWP>(a, B, stream);
+    float* ain = TRWP ? A[0] : A[(k + 1) & 1];
+    float* aout = TRWP ? A[0] : A[k & 1];
+    if (TRWP) {
+      for (int r = R - 1; r >= 0; --r) {  // directions in reverse (autodiff.hpp:147)
+        AccArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), p, q, k, grad_cost,
+                  ain, aout, grads->weight_planes, gvacc, desc.get()};
+        ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
+        cuda_check(launch_bwd_trwp(a, B, stream), "bwd_split_kernel launch");
+      }
+    } else {
+      AccArgs a{g, pot, lines + topo->every_start, int(topo->every_line.size()), p, q, k, grad_cost,
+                ain, aout, isgmr_dw ? dwr : nullptr, gvacc, desc.get()};
+      ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
+      cuda_check(launch_bwd_isgmr(a, B, stream), "bwd_split_kernel launch");
     }
-    if (!TRWP) std::swap(gm, gnext);
+    {
+      ProfScope ps(stream, MRF_KCLASS_AUX);
+      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, TRWP ? pr->rho_planes : nullptr, g,
+                                                           grads->unary);
+      cuda_check(cudaGetLastError(), "dtheta_acc launch");
+    }
+  }
+  if (isgmr_dw) {
+    ProfScope ps(stream, MRF_KCLASS_AUX);
+    combine_dw_kernel<<<int(std::min<int64_t>(148 * 4, (int64_t(B) * (R / 2) * N + 255) / 256)), 256, 0, stream>>>(
+        B, R, N, dwr, grads->weight_planes);
+    cuda_check(cudaGetLastError(), "combine_dw launch");
   }
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
@@ -507,7 +519,9 @@ size_t mrf_backward_workspace_bytes(mrf_topology_t topo, const mrf_problem_f32* 
   (void)iterations;
   if (!topo || !prob) return 0;
   const size_t mb = align_up(messages_bytes(topo, prob));
-  return mb * (engine == MRF_ENGINE_ISGMR ? 2 : 1) + align_up(gvacc_bytes(prob));
+  if (engine == MRF_ENGINE_ISGMR)
+    return mb * 2 + align_up(gvacc_bytes(prob)) + align_up(dwr_bytes(prob, topo->host.num_dirs(), topo->host.nodes()));
+  return mb + align_up(gvacc_bytes(prob));
 }
 
 int mrf_isgmr_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const uint8_t* p,
