@@ -80,6 +80,7 @@ struct FwdArgs {
   int k;
   const PairDesc* desc;
   int band2_launched;  // fwd_band2_kernel covers banded D == 2 in this sweep
+  int bandw_max;       // fwd_bandw_kernel covers banded 2 < D <= bandw_max (0: not launched)
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(128) fwd_warp_kernel(FwdArgs a) {
   if (a.desc->banded) {
     if (a.desc->D == 2) {
       if (!a.band2_launched) fwd_sweep_lines<EPL, TRWP, 2>(a, ws);
-    } else {
+    } else if (!(a.desc->D > 2 && a.desc->D <= a.bandw_max)) {
       fwd_sweep_lines<EPL, TRWP, 1>(a, ws);
     }
   } else {

@@ -79,6 +79,51 @@ def test_random_problems_bit_exact(engine, case):
     assert_grads_close(g, gref)
 
 
+WIDE = [
+    # H, W, L, conn, K, pairwise (kind, param), per_edge
+    (9, 11, 16, 4, 2, ("tl", 3.0), False),
+    (7, 13, 64, 8, 2, ("tl", 6.0), True),
+    (8, 7, 100, 4, 2, ("tq", 40.0), False),
+    (6, 9, 192, 4, 2, ("tl", 15.0), False),
+    (5, 6, 256, 4, 3, ("tq", 200.0), False),
+    (10, 8, 21, 8, 2, ("tq", 9.0), True),
+    (7, 7, 33, 4, 2, ("tl", 16.0), False),
+    (6, 8, 40, 4, 2, ("tl", 17.0), False),   # D = 17 > 16: generic banded path
+    (6, 8, 12, 4, 2, ("potts", 1.0), False),  # D = 1
+]
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", WIDE, ids=[f"{c[5][0]}{c[5][1]:g}L{c[2]}c{c[3]}" for c in WIDE])
+def test_wide_band_bit_exact(engine, case):
+    """Banded V with D != 2 (truncated linear / quadratic, Potts): the
+    wide-band forward (2 < D <= 16) and the generic banded path."""
+    H, W, L, conn, K, (kind, prm), per_edge = case
+    un, _, wc, planes = WL.random_problem(H, W, L, conn, seed=H * 7 + L, per_edge=per_edge)
+    V = {"tl": WL.truncated_linear, "tq": WL.truncated_quadratic}[kind](L, prm) if kind != "potts" else WL.potts(L)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    mrf = to_mrf(pr)
+    f = gpu_forward(engine, mrf, K)
+    assert_forward_equal(f, ref)
+    _, _, gc = O.soft_head(ref.cost, np.random.default_rng(L).uniform(0.25, L - 1.25, H * W), L)
+    g = gpu_backward(engine, mrf, f, gc)
+    assert_grads_close(g, O.backward(engine, pr, K, ref.p, ref.q, gc))
+
+
+def test_c5_shaped_integer_ties():
+    """C5 recipe (integer TQ denoising, V = min(d^2, 200), w = 25: exact
+    arithmetic, maximal ties) on a small grid, both engines."""
+    H, W, L = 24, 20, 256
+    un = WL.denoise_tq(H, W, L, seed=5)
+    V = WL.truncated_quadratic(L, 200.0)
+    for engine in ("isgmr", "trwp"):
+        pr = O.Problem(H, W, L, 4, un, V, 25.0, None, 0.5, None)
+        ref = O.forward(engine, pr, 3)
+        f = gpu_forward(engine, to_mrf(pr), 3)
+        assert_forward_equal(f, ref)
+
+
 @pytest.mark.parametrize("engine", ["isgmr", "trwp"])
 def test_batch_images_independent(engine):
     H, W, L, conn, K, B = 11, 9, 21, 4, 2, 3
