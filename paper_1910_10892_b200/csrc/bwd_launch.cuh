@@ -3,16 +3,17 @@
 #pragma once
 
 #include "bwd_common.cuh"
+#include "bwd_small.cuh"
 #include "bwd_split.cuh"
 #include "launch.hpp"
 
 namespace mrf {
 
-template <int EPL, bool TRWP, int RT, bool FULL, bool BAND>
+template <int EPL, bool TRWP, int RT, bool FULL, int MODE>
 static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   constexpr int NPRE = kSplitPre;
-  const int smem = split_smem_floats(EPL, acc_rows(TRWP, a.g.R), NPRE) * int(sizeof(float));
-  auto kern = bwd_split_kernel<EPL, TRWP, RT, FULL, NPRE, BAND>;
+  const int smem = split_smem_floats(EPL, acc_rows(TRWP, a.g.R), NPRE, MODE == 2) * int(sizeof(float));
+  auto kern = bwd_split_kernel<EPL, TRWP, RT, FULL, NPRE, MODE>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = a.nlines < 65535 ? a.nlines : 65535;
@@ -20,13 +21,14 @@ static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// The pairwise strategy is known on the device only: both variants are
-// launched and the one that does not own the sweep exits at once.
+// The pairwise strategy is known on the device only: every mode is launched
+// and the instantiations that do not own the sweep exit at once.
 template <int EPL, bool TRWP, int RT, bool FULL>
 static cudaError_t run_split(const AccArgs& a, int batch, cudaStream_t s) {
-  cudaError_t e = run_split1<EPL, TRWP, RT, FULL, true>(a, batch, s);
-  if (e != cudaSuccess) return e;
-  return run_split1<EPL, TRWP, RT, FULL, false>(a, batch, s);
+  cudaError_t e = run_split1<EPL, TRWP, RT, FULL, 1>(a, batch, s);
+  if (e == cudaSuccess) e = run_split1<EPL, TRWP, RT, FULL, 2>(a, batch, s);
+  if (e == cudaSuccess) e = run_split1<EPL, TRWP, RT, FULL, 0>(a, batch, s);
+  return e;
 }
 
 template <int EPL, bool TRWP>
@@ -37,9 +39,28 @@ static cudaError_t run_split_r(const AccArgs& a, int batch, cudaStream_t s) {
   return run_split<EPL, TRWP, 0, false>(a, batch, s);
 }
 
+// L <= 32: one warp per scanline, lane = label (bwd_small.cuh)
+template <bool TRWP, int RT>
+static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
+  const int wpc = 4;
+  const int smem = small_warp_floats(acc_rows(TRWP, a.g.R)) * int(sizeof(float)) * wpc;
+  auto kern = bwd_small_kernel<TRWP, RT>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <bool TRWP>
 static cudaError_t launch_bwd_sweep(const AccArgs& a, int batch, cudaStream_t s) {
   if (a.nlines == 0) return cudaSuccess;
+  // L <= 32 with many lines: one warp per line; few lines: warp-specialised
+  if (a.g.L <= 32 && int64_t(a.nlines) * batch >= 148 * 16) {
+    if (a.g.R == 4) return run_small<TRWP, 4>(a, batch, s);
+    if (a.g.R == 8) return run_small<TRWP, 8>(a, batch, s);
+    return run_small<TRWP, 0>(a, batch, s);
+  }
   switch (epl_for(a.g.L)) {
     case 1: return run_split_r<1, TRWP>(a, batch, s);
     case 2: return run_split_r<2, TRWP>(a, batch, s);

@@ -69,23 +69,45 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // Slot layout (floats), LS = 32*EPL:
-//   X[LS] B[LS] ACC[LS] CIN[LS] P[8*EPL words] MASK[32] OTH[16*EPL words] SC[8]
+//   X[LS] B[LS] ACC[LS] CIN[LS] P[8*EPL words] MASK[32] OTH[16*EPL words] WM[LS words] SC[8]
+// WM (window mode): per target label mu, bit s + kWin set when source
+// mu + s (|s| <= kWin) has p == mu.
 template <int EPL>
 struct SlotLayout {
   static constexpr int LS = 32 * EPL;
   static constexpr int X = 0, B = LS, ACC = 2 * LS, CIN = 3 * LS, P = 4 * LS, MASK = P + 8 * EPL,
-                       OTH = MASK + 32, SC = OTH + 16 * EPL, SIZE = (SC + 8 + 3) / 4 * 4;
+                       OTH = MASK + 32, WM = OTH + 16 * EPL, SC = WM + LS, SIZE = (SC + 8 + 3) / 4 * 4;
 };
+constexpr int kWin = 15;  // window mode: targets within +-kWin labels of the source are gathered
 // scalar words of a slot
 enum { SC_Q = 0, SC_S = 1, SC_MAIN = 2, SC_NOTH = 3, SC_W = 4, SC_RHO = 5 };
 
-__host__ __device__ constexpr int split_slot_floats(int EPL) { return (152 * EPL + 40 + 3) / 4 * 4; }
+__host__ __device__ constexpr int split_slot_floats(int EPL) { return (184 * EPL + 40 + 3) / 4 * 4; }
 // PRE ring stage: NR rows + p bytes (8*EPL words) + scalars {q word, w, rho, pad} + rho_d[NR] per lane
 __host__ __device__ constexpr int split_stage_floats(int EPL, int NR) { return NR * 32 * EPL + 8 * EPL + 4 + 32 * NR; }
-// slots + PRE rings + dw parking [32][33] + chain reduction [32] + 3*NS mbarriers
-__host__ __device__ constexpr int split_smem_floats(int EPL, int NR, int npre) {
+// slots + PRE rings + dw parking [32][33] + chain reduction [32] + 3*NS
+// mbarriers (+ window mode: the chain's padded carry row and POST's
+// near-band dV accumulators [32*EPL][2*kWin+1])
+__host__ __device__ constexpr int split_smem_floats(int EPL, int NR, int npre, bool win) {
   return kSplitSlots * split_slot_floats(EPL) + npre * kPreStages * split_stage_floats(EPL, NR) + 32 * 33 + 32 +
-         3 * kSplitSlots * 2 + 8;
+         3 * kSplitSlots * 2 + 8 + (win ? 32 * (EPL + 1) + 32 * EPL * (2 * kWin + 1) : 0);
+}
+// padded row index (lane stride EPL+1 words: conflict-free neighbour gathers)
+template <int EPL>
+__device__ __forceinline__ int pidx(int l) { return l + l / EPL; }
+
+// acc[i] += sum over the sources of target l0+i recorded in wm[i] of val(source)
+template <int EPL, class F>
+__device__ __forceinline__ void window_gather(float (&acc)[EPL], const uint32_t (&wm)[EPL], int l0, F val) {
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) {
+    uint32_t m = wm[i];
+    while (m) {
+      const int k = __ffs(m) - 1;
+      m &= m - 1;
+      acc[i] = fadd(acc[i], val(l0 + i + k - kWin));
+    }
+  }
 }
 
 // Store a lane's EPL floats to shared memory (vectorised).
@@ -117,7 +139,7 @@ __device__ __forceinline__ bool bit(uint32_t w, int k) { return (w >> k) & 1u; }
 // registers and neighbour shuffles; the main far group through a warp
 // reduction (shared memory `red`, 32 floats, 16 B aligned); other far pairs
 // one shuffle each.
-template <int EPL>
+template <int EPL, bool NEAR = true>
 __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[EPL], uint32_t mword, int main_t,
                                             int noth, const uint16_t* oth, float* red, int lane) {
   float nm[EPL], np[EPL], part = 0.0f;
@@ -137,11 +159,13 @@ __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[
     red[lane] = part;
     __syncwarp();
   }
+  if (NEAR) {
 #pragma unroll
-  for (int i = 0; i < EPL; ++i) {
-    const float m1 = i + 1 < EPL ? nm[i + 1 < EPL ? i + 1 : 0] : mn;
-    const float p1 = i > 0 ? np[i > 0 ? i - 1 : 0] : pn;
-    acc[i] = fadd(fadd(fadd(acc[i], bit(mword, 8 + i) ? v[i] : 0.0f), m1), p1);
+    for (int i = 0; i < EPL; ++i) {
+      const float m1 = i + 1 < EPL ? nm[i + 1 < EPL ? i + 1 : 0] : mn;
+      const float p1 = i > 0 ? np[i > 0 ? i - 1 : 0] : pn;
+      acc[i] = fadd(fadd(fadd(acc[i], bit(mword, 8 + i) ? v[i] : 0.0f), m1), p1);
+    }
   }
   if (main_t >= 0) {
     float s[8];
@@ -167,11 +191,19 @@ __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[
   }
 }
 
-template <int EPL, bool TRWP, int RT, bool FULL, int NPRE, bool BAND>
+// MODE 1: banded D <= 2 (near targets l-1 / l / l+1 through shuffles);
+// MODE 2: window (banded D <= 16, or any V with L <= 32): targets within
+// +-kWin gathered through per-target source masks; MODE 0: everything else.
+__host__ __device__ inline int split_mode(int banded, int D, int L) {
+  return (banded && D <= 2) ? 1 : (((banded && D <= 16) || (!banded && L <= 32)) ? 2 : 0);
+}
+
+template <int EPL, bool TRWP, int RT, bool FULL, int NPRE, int MODE>
 __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
   const bool band = a.desc->banded != 0;
   const int Dband = a.desc->D;
-  if ((band && Dband <= 2) != BAND) return;  // the other instantiation owns this sweep
+  if (split_mode(band, Dband, a.g.L) != MODE) return;  // another instantiation owns this sweep
+  constexpr bool BAND = MODE == 1, WIN = MODE == 2;
   extern __shared__ __align__(16) float smem[];
   using SL = SlotLayout<EPL>;
   constexpr int NRMAX = RT ? acc_rows(TRWP, RT) : 16;
@@ -190,6 +222,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
   float* s_wp = pre_ring + NPRE * kPreStages * stage_f;      // [32][33] POST dw parking
   float* s_red = s_wp + 32 * 33;                             // [32] CHAIN reduction
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_red + 32);  // full[NS], done[NS], empty[NS]
+  float* s_c = reinterpret_cast<float*>(bars + 3 * kSplitSlots + 4);  // WIN: chain carry row (padded)
+  float* s_dv = s_c + 32 * (EPL + 1);                                    // WIN: [32*EPL][2*kWin+1]
   uint64_t* bar_full = bars;
   uint64_t* bar_done = bars + kSplitSlots;
   uint64_t* bar_empty = bars + 2 * kSplitSlots;
@@ -392,7 +426,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
 
         // ---- decode p: near codes, far targets
         int mu[EPL];
-        bool far[EPL];
+        bool far[EPL], near[EPL];
         float lsum = 0.0f;
         uint32_t mword = 0;
         int kmn = 0x7fffffff, kmx = -1;
@@ -403,10 +437,13 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
           lsum = fadd(lsum, x[i]);
           mu[i] = valid ? int(prow[i]) : l0 + i;
           const int d = mu[i] - (l0 + i);
-          far[i] = valid && uint32_t(d + 1) > 2u;
-          mword |= (valid && d == -1 ? 1u : 0u) << i;
-          mword |= (valid && d == 0 ? 1u : 0u) << (8 + i);
-          mword |= (valid && d == 1 ? 1u : 0u) << (16 + i);
+          near[i] = valid && uint32_t(d + (WIN ? kWin : 1)) <= uint32_t(WIN ? 2 * kWin : 2);
+          far[i] = valid && !near[i];
+          if (!WIN) {
+            mword |= (valid && d == -1 ? 1u : 0u) << i;
+            mword |= (valid && d == 0 ? 1u : 0u) << (8 + i);
+            mword |= (valid && d == 1 ? 1u : 0u) << (16 + i);
+          }
           kmn = far[i] ? min(kmn, mu[i]) : kmn;
           kmx = far[i] ? max(kmx, mu[i]) : kmx;
         }
@@ -474,7 +511,23 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         float B[EPL];
 #pragma unroll
         for (int i = 0; i < EPL; ++i) B[i] = 0.0f;
-        scatter_row<EPL>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
+        if (WIN) {
+          uint32_t* wmk = reinterpret_cast<uint32_t*>(sl + SL::WM);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) wmk[l0 + i] = 0u;
+          sts_slice<EPL>(sl + SL::X + l0, x);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < EPL; ++i)
+            if (near[i]) atomicOr(wmk + mu[i], 1u << (kWin - (mu[i] - (l0 + i))));
+          __syncwarp();
+          uint32_t wm[EPL];
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) wm[i] = wmk[l0 + i];
+          const float* xr = sl + SL::X;
+          window_gather<EPL>(B, wm, l0, [&](int l) { return xr[l]; });
+        }
+        scatter_row<EPL, !WIN>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
         {
           int muq = mu[0];
 #pragma unroll
@@ -487,7 +540,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         }
         __syncwarp();
         PMARK(4);
-        sts_slice<EPL>(sl + SL::X + l0, x);
+        if (!WIN) sts_slice<EPL>(sl + SL::X + l0, x);
         sts_slice<EPL>(sl + SL::B + l0, B);
         if (!BAND) {
           uint8_t* pb = reinterpret_cast<uint8_t*>(sl + SL::P);
@@ -526,8 +579,18 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         const uint32_t mword = reinterpret_cast<const uint32_t*>(sl + SL::MASK)[lane];
         float acc[EPL];
         lds_slice<EPL>(acc, sl + SL::B + l0);
-        scatter_row<EPL>(acc, carry, mword, main_t, noth, reinterpret_cast<const uint16_t*>(sl + SL::OTH), s_red,
-                         lane);
+        if (WIN) {
+          __syncwarp();  // the previous step's gathers are done
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) s_c[pidx<EPL>(l0 + i)] = carry[i];
+          uint32_t wm[EPL];
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) wm[i] = reinterpret_cast<const uint32_t*>(sl + SL::WM)[l0 + i];
+          __syncwarp();
+          window_gather<EPL>(acc, wm, l0, [&](int l) { return s_c[pidx<EPL>(l)]; });
+        }
+        scatter_row<EPL, !WIN>(acc, carry, mword, main_t, noth, reinterpret_cast<const uint16_t*>(sl + SL::OTH), s_red,
+                               lane);
         sts_slice<EPL>(sl + SL::CIN + l0, carry);
         sts_slice<EPL>(sl + SL::ACC + l0, acc);
         mbar_arrive(bar_done + slot);
@@ -547,6 +610,10 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
       for (int i = 0; i < EPL; ++i) zero[i] = 0.0f;
       // the tail is no edge's prev: its plane-r row is zero
       stg_slice<EPL>(aout_r + o_first + nsteps * stL, l0, zero, nvalid, L);
+      if (WIN && gs0 == 0) {
+        for (int t = lane; t < 32 * EPL * (2 * kWin + 1); t += 32) s_dv[t] = 0.0f;
+        __syncwarp();
+      }
       // dV partials (w folded in at flush when w is constant): near diagonal
       // (mu = l-1, l, l+1) and the main far target while it repeats
       float vacc[EPL][3], fval[EPL];
@@ -618,18 +685,28 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
           }
           if (do_w) wpart = fadd(fadd(fmul(gb0, s0), fmul(gb1, s1)), fmul(gbD, sf));
         } else {
+          const uint8_t* pb = reinterpret_cast<const uint8_t*>(sl + SL::P);
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
             const float ga = wpl ? fmul(gg[i], w) : gg[i];
-            const bool cm = bit(mword, i), c0 = bit(mword, 8 + i), cp = bit(mword, 16 + i), cf = bit(mword, 24 + i);
-            vacc[i][0] = fadd(vacc[i][0], cm ? ga : 0.0f);
-            vacc[i][1] = fadd(vacc[i][1], c0 ? ga : 0.0f);
-            vacc[i][2] = fadd(vacc[i][2], cp ? ga : 0.0f);
+            const bool cf = bit(mword, 24 + i);
+            const int l = l0 + i;
+            const bool valid = FULL || i < nvalid;
+            const int m = valid ? int(pb[l]) : l;
+            const int d = m - l;
+            if (WIN) {
+              // near-band dV partial of (m, l): shared accumulator, one owner lane per label
+              if (valid && d >= -kWin && d <= kWin && ga != 0.0f) atomicAdd(s_dv + l * (2 * kWin + 1) + d + kWin, ga);
+            } else {
+              const bool cm = bit(mword, i), c0 = bit(mword, 8 + i), cp = bit(mword, 16 + i);
+              vacc[i][0] = fadd(vacc[i][0], cm ? ga : 0.0f);
+              vacc[i][1] = fadd(vacc[i][1], c0 ? ga : 0.0f);
+              vacc[i][2] = fadd(vacc[i][2], cp ? ga : 0.0f);
+            }
             fval[i] = fadd(fval[i], cf ? ga : 0.0f);
-            if (do_w && (FULL || i < nvalid)) {
-              const int m = reinterpret_cast<const uint8_t*>(sl + SL::P)[l0 + i];
-              const float vv = (gg[i] != 0.0f) ? __ldg(a.pot.V + m * vs_mu + (l0 + i) * vs_l) : 0.0f;
-              wpart = gg[i] != 0.0f ? fadd(wpart, fmul(gg[i], vv)) : wpart;
+            if (do_w && valid && gg[i] != 0.0f) {
+              const float vv = band ? __ldg(gband + min(abs(d), Dband)) : __ldg(a.pot.V + m * vs_mu + l * vs_l);
+              wpart = fadd(wpart, fmul(gg[i], vv));
             }
           }
         }
@@ -651,13 +728,26 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         mbar_arrive(bar_empty + slot);
       }
       if (fkey >= 0) flush_far();
+      if (WIN) {
+        __syncwarp();
+        for (int t = lane; t < L * (2 * kWin + 1); t += 32) {
+          const float v = s_dv[t];
+          if (v != 0.0f) {
+            const int l = t / (2 * kWin + 1), m = l + t % (2 * kWin + 1) - kWin;
+            red_add_global(gvacc + m * L + l, fmul(v, wfold));
+            s_dv[t] = 0.0f;
+          }
+        }
+        __syncwarp();
+      } else {
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) {
-        const int l = l0 + i;
+        for (int i = 0; i < EPL; ++i) {
+          const int l = l0 + i;
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-          const int m = l + t - 1;
-          if (l < L && m >= 0 && m < L && vacc[i][t] != 0.0f) red_add_global(gvacc + m * L + l, fmul(vacc[i][t], wfold));
+          for (int t = 0; t < 3; ++t) {
+            const int m = l + t - 1;
+            if (l < L && m >= 0 && m < L && vacc[i][t] != 0.0f) red_add_global(gvacc + m * L + l, fmul(vacc[i][t], wfold));
+          }
         }
       }
     }
