@@ -139,7 +139,7 @@ __device__ __forceinline__ bool bit(uint32_t w, int k) { return (w >> k) & 1u; }
 // registers and neighbour shuffles; the main far group through a warp
 // reduction (shared memory `red`, 32 floats, 16 B aligned); other far pairs
 // one shuffle each.
-template <int EPL, bool NEAR = true>
+template <int EPL, bool NEAR = true, bool SMEM_RED = true>
 __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[EPL], uint32_t mword, int main_t,
                                             int noth, const uint16_t* oth, float* red, int lane) {
   float nm[EPL], np[EPL], part = 0.0f;
@@ -154,7 +154,7 @@ __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[
   float pn = __shfl_up_sync(0xffffffffu, np[EPL - 1], 1);
   mn = lane < 31 ? mn : 0.0f;
   pn = lane > 0 ? pn : 0.0f;
-  if (main_t >= 0) {
+  if (SMEM_RED && main_t >= 0) {
     __syncwarp();
     red[lane] = part;
     __syncwarp();
@@ -168,13 +168,18 @@ __device__ __forceinline__ void scatter_row(float (&acc)[EPL], const float (&v)[
     }
   }
   if (main_t >= 0) {
-    float s[8];
+    float F;
+    if (SMEM_RED) {
+      float s[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const float4 q4 = reinterpret_cast<const float4*>(red)[t];
-      s[t] = fadd(fadd(q4.x, q4.y), fadd(q4.z, q4.w));
+      for (int t = 0; t < 8; ++t) {
+        const float4 q4 = reinterpret_cast<const float4*>(red)[t];
+        s[t] = fadd(fadd(q4.x, q4.y), fadd(q4.z, q4.w));
+      }
+      F = fadd(fadd(fadd(s[0], s[1]), fadd(s[2], s[3])), fadd(fadd(s[4], s[5]), fadd(s[6], s[7])));
+    } else {
+      F = warp_sum_f(part);  // throughput role: fewer instructions than the shared-memory tree
     }
-    const float F = fadd(fadd(fadd(s[0], s[1]), fadd(s[2], s[3])), fadd(fadd(s[4], s[5]), fadd(s[6], s[7])));
     const int im = main_t - lane * EPL;
 #pragma unroll
     for (int i = 0; i < EPL; ++i)
@@ -481,6 +486,23 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
 #ifdef MRF_SPLIT_PROF
         t_c0 += clock64() - tc0;
 #endif
+        // B = scatter(x) - S_x e_{p_q}: needs no slot unless the window masks
+        // or the other-pairs list live in it
+        const uint8_t* prow0 = prow - l0;  // staged p row, label 0
+        float B[EPL];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) B[i] = 0.0f;
+        auto qfix = [&]() {
+          const int im = int(prow0[qv]) - l0;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i)
+            if (im == i) B[i] = fsub(B[i], S);
+        };
+        const bool early = !WIN && !split;
+        if (early) {
+          scatter_row<EPL, true, false>(B, x, mword, main_t, 0, nullptr, nullptr, lane);
+          qfix();
+        }
         // ---- wait for the slot, then publish
         const uint32_t gs = gs0 + uint32_t(s);
         const int slot = int(gs % kSplitSlots);
@@ -507,10 +529,6 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
 #ifdef MRF_SPLIT_PROF
         n_oth += noth;
 #endif
-        // B = scatter(x) - S_x e_{p_q}
-        float B[EPL];
-#pragma unroll
-        for (int i = 0; i < EPL; ++i) B[i] = 0.0f;
         if (WIN) {
           uint32_t* wmk = reinterpret_cast<uint32_t*>(sl + SL::WM);
 #pragma unroll
@@ -527,16 +545,9 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
           const float* xr = sl + SL::X;
           window_gather<EPL>(B, wm, l0, [&](int l) { return xr[l]; });
         }
-        scatter_row<EPL, !WIN>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
-        {
-          int muq = mu[0];
-#pragma unroll
-          for (int i = 1; i < EPL; ++i) muq = (qv - l0 == i) ? mu[i] : muq;
-          muq = __shfl_sync(0xffffffffu, muq, qv / EPL);
-          const int im = muq - l0;
-#pragma unroll
-          for (int i = 0; i < EPL; ++i)
-            if (im == i) B[i] = fsub(B[i], S);
+        if (!early) {
+          scatter_row<EPL, !WIN>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
+          qfix();
         }
         __syncwarp();
         PMARK(4);
@@ -669,8 +680,11 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         }
         float wpart = 0.0f;
         if (BAND) {
-          // dw = g(0) sum_{d=0} g + g(1) sum_{|d|=1} g + g(D) sum_far g
-          float s0 = 0.0f, s1 = 0.0f, sf = 0.0f;
+          // dw = g(0) s0 + g(1) s1 + g(D) (sum_l g_l - s0 - s1) with s0 / s1 the
+          // sums over p_l == l / |p_l - l| == 1, and sum_l g_l = 0 (the
+          // reparametrised row sums to zero: dropping it changes dw only at the
+          // rounding level of the reference's own sum)
+          float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
             const float ga = wpl ? fmul(gg[i], w) : gg[i];  // dV addend (w folded later if constant)
@@ -681,9 +695,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
             fval[i] = fadd(fval[i], cf ? ga : 0.0f);
             s0 = fadd(s0, c0 ? gg[i] : 0.0f);
             s1 = fadd(s1, (cm || cp) ? gg[i] : 0.0f);
-            sf = (cm || c0 || cp) ? sf : fadd(sf, gg[i]);  // every far label (main or not)
           }
-          if (do_w) wpart = fadd(fadd(fmul(gb0, s0), fmul(gb1, s1)), fmul(gbD, sf));
+          if (do_w) wpart = fadd(fmul(fsub(gb0, gbD), s0), fmul(fsub(gb1, gbD), s1));
         } else {
           const uint8_t* pb = reinterpret_cast<const uint8_t*>(sl + SL::P);
 #pragma unroll
