@@ -56,9 +56,10 @@ struct AccArgs {
   float* gw;         // TRWP: [B][R/2][N] (family planes); ISGMR: [B][R][N] per direction; or null
   float* gvacc;      // [B][kVRep][2][L][L]
   const PairDesc* desc;
+  float* dtheta;     // TRWP direction 0: dtheta += rho_d A[d] of the iteration, fused (else null)
 };
 
-// row slots: TRWP R-1 planes (+ dc at k == K-1 needs at most R in total), ISGMR R-2 planes or dc
+// row slots: TRWP R-1 planes (+ dc at k == K-1: at most R), ISGMR R-2 planes or dc
 __host__ __device__ constexpr int acc_rows(bool trwp, int R) { return trwp ? R : (R - 2 > 1 ? R - 2 : 1); }
 
 __device__ __forceinline__ float warp_sum_f(float v) {

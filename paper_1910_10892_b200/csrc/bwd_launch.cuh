@@ -56,7 +56,7 @@ template <bool TRWP>
 static cudaError_t launch_bwd_sweep(const AccArgs& a, int batch, cudaStream_t s) {
   if (a.nlines == 0) return cudaSuccess;
   // L <= 32 with many lines: one warp per line; few lines: warp-specialised
-  if (a.g.L <= 32 && int64_t(a.nlines) * batch >= 148 * 16) {
+  if (bwd_uses_small(a.g.L, a.nlines, batch)) {
     if (a.g.R == 4) return run_small<TRWP, 4>(a, batch, s);
     if (a.g.R == 8) return run_small<TRWP, 8>(a, batch, s);
     return run_small<TRWP, 0>(a, batch, s);

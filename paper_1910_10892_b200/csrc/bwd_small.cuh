@@ -102,6 +102,9 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
         if (d != r && d != opp) push(d);
     }
     const int a0 = first ? 1 : 0;
+    const int npl = nrows;  // plane rows end here
+    const bool fuse = TRWP && a.dtheta != nullptr;
+    float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
     const uint32_t ebase = uint32_t(a.k) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
 
     auto issue = [&](int s) {
@@ -144,6 +147,8 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     // the tail is no edge's prev: its plane-r row is zero
     if (valid) aoutb[size_t(r) * NL + o_first + nsteps * stL] = 0.0f;
     float carry = 0.0f;
+    // fused unary gradient: dtheta(cur) loaded one step ahead
+    float dtn = (fuse && valid && nsteps > 0) ? __ldcg(dthb + o_first + nsteps * stL + lane) : 0.0f;
 
     for (int s = 0; s < nsteps; ++s) {
       if (s + kStages - 1 < nsteps) issue(s + kStages - 1);
@@ -160,24 +165,25 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
       const float rho = TRWP ? (rpl ? xs[2] : a.pot.rho) : 1.0f;
 
       // ---- x (bwd_common.cuh rules) and row = x + carry
-      float x = 0.0f;
+      float x = 0.0f, rsum = 0.0f;
       if (!rpl) {
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr)
-          if (rr >= a0 && rr < nrows) x = fadd(x, stg[rr * 32 + lane]);
-        if (TRWP && nrows > a0) {
-          x = fmul(a.pot.rho, x);
+          if (rr >= a0 && rr < npl) x = fadd(x, stg[rr * 32 + lane]);
+        if (TRWP && npl > a0) {
+          rsum = x = fmul(a.pot.rho, x);
           if (opp_slot >= 0) x = fsub(x, stg[opp_slot * 32 + lane]);
         }
         if (first) x = fadd(stg[lane], x);
       } else {
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr) {
-          if (rr >= nrows) continue;
+          if (rr >= npl) continue;
           const float t = stg[rr * 32 + lane];
           float c = t;
           if (sd[rr] >= 0) {
             c = fmul(xs[4 + rr], t);
+            rsum = fadd(rsum, c);
             if (sd[rr] == opp) c = fsub(c, t);
           }
           x = fadd(x, c);
@@ -213,6 +219,12 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
         if (k >= 0) acc = fadd(acc, s_g[k]);
       }
       if (valid) aoutb[size_t(r) * NL + o_first + (j - 1) * stL] = acc;
+      // fused unary gradient: dtheta(cur) += sum_d rho_d A[d](cur) + this sweep's share
+      if (fuse && valid) {
+        const float dnew = fadd(fadd(dtn, rsum), carry);
+        if (s + 1 < nsteps) dtn = __ldcg(dthb + o_first + (j - 1) * stL + lane);
+        dthb[o_first + j * stL + lane] = dnew;
+      }
       carry = TRWP ? fmul(rho, acc) : acc;
 
       // ---- dV (shared accumulator, w folded per edge) and dw of this edge
@@ -236,6 +248,20 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     }
     cp_wait<0>();
     __syncwarp();
+    if (fuse && valid) {  // the head is no edge's cur: its rows are read here
+      const int head = ld.first;
+      float hs = 0.0f;
+      for (int d = 1; d < R; ++d) {
+        float rd = a.pot.rho;
+        if (rpl) {
+          const int wn = (d & 1) ? head + g.node_step[d] : head;
+          rd = __ldg(a.pot.rho_planes + (size_t(b) * (R / 2) + (d >> 1)) * N + min(max(wn, 0), N - 1));
+        }
+        hs = fadd(hs, fmul(rd, __ldcg(ainb + size_t(d) * NL + size_t(head) * L)));
+      }
+      float* dst = dthb + size_t(head) * L + lane;
+      *dst = fadd(fadd(*dst, hs), carry);
+    }
     // flush this line's dV partials (lane l owns column l)
     if (valid) {
       for (int m = 0; m < L; ++m) {

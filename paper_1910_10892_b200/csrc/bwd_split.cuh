@@ -69,20 +69,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // Slot layout (floats), LS = 32*EPL:
-//   X[LS] B[LS] ACC[LS] CIN[LS] P[8*EPL words] MASK[32] OTH[16*EPL words] WM[LS words] SC[8]
+//   X[LS] B[LS] ACC[LS] CIN[LS] P[8*EPL words] MASK[32] OTH[16*EPL words] WM[LS words] DT[LS] SC[8]
+// DT (fused dtheta sweep): dtheta(cur) + sum_d rho_d A[d](cur), the carry is added by POST.
 // WM (window mode): per target label mu, bit s + kWin set when source
 // mu + s (|s| <= kWin) has p == mu.
 template <int EPL>
 struct SlotLayout {
   static constexpr int LS = 32 * EPL;
   static constexpr int X = 0, B = LS, ACC = 2 * LS, CIN = 3 * LS, P = 4 * LS, MASK = P + 8 * EPL,
-                       OTH = MASK + 32, WM = OTH + 16 * EPL, SC = WM + LS, SIZE = (SC + 8 + 3) / 4 * 4;
+                       OTH = MASK + 32, WM = OTH + 16 * EPL, DT = WM + LS, SC = DT + LS, SIZE = (SC + 8 + 3) / 4 * 4;
 };
 constexpr int kWin = 15;  // window mode: targets within +-kWin labels of the source are gathered
 // scalar words of a slot
 enum { SC_Q = 0, SC_S = 1, SC_MAIN = 2, SC_NOTH = 3, SC_W = 4, SC_RHO = 5 };
 
-__host__ __device__ constexpr int split_slot_floats(int EPL) { return (184 * EPL + 40 + 3) / 4 * 4; }
+__host__ __device__ constexpr int split_slot_floats(int EPL) { return (216 * EPL + 40 + 3) / 4 * 4; }
 // PRE ring stage: NR rows + p bytes (8*EPL words) + scalars {q word, w, rho, pad} + rho_d[NR] per lane
 __host__ __device__ constexpr int split_stage_floats(int EPL, int NR) { return NR * 32 * EPL + 8 * EPL + 4 + 32 * NR; }
 // slots + PRE rings + dw parking [32][33] + chain reduction [32] + 3*NS
@@ -204,7 +205,9 @@ __host__ __device__ inline int split_mode(int banded, int D, int L) {
 }
 
 template <int EPL, bool TRWP, int RT, bool FULL, int NPRE, int MODE>
-__global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
+// 3 CTAs per SM: few long scanlines (KITTI rows: 375 lines) run in one wave,
+// many lines get 15 warps per SM to hide latency (measured on C2 and C3)
+__global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a) {
   const bool band = a.desc->banded != 0;
   const int Dband = a.desc->D;
   if (split_mode(band, Dband, a.g.L) != MODE) return;  // another instantiation owns this sweep
@@ -303,6 +306,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
           if (d != r && d != opp) push(d);
       }
       const int a0 = first ? 1 : 0;  // first plane slot
+      const int npl = nrows;         // plane rows end here
+      const bool fuse = TRWP && a.dtheta != nullptr;
       int soff[NRMAX];
 #pragma unroll
       for (int rr = 0; rr < NRMAX; ++rr) soff[rr] = sd[rr] < 0 ? 0 : sd[rr] * NL;
@@ -385,19 +390,20 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         float x[EPL], tv[EPL];
 #pragma unroll
         for (int i = 0; i < EPL; ++i) x[i] = 0.0f;
+        float rsum[EPL];  // fused dtheta: sum_d rho_d A[d](cur)
         if (!rpl) {
           // uniform rho: x = dc + rho * sum_d A_d - A_opp (TRWP) / dc or sum_d A_d (ISGMR)
 #pragma unroll
           for (int rr = 0; rr < NRMAX; ++rr) {
-            if (rr >= a0 && rr < nrows) {
+            if (rr >= a0 && rr < npl) {
               lds_slice<EPL>(tv, stg + rr * LS + l0);
 #pragma unroll
               for (int i = 0; i < EPL; ++i) x[i] = fadd(x[i], tv[i]);
             }
           }
-          if (TRWP && nrows > a0) {
+          if (TRWP && npl > a0) {
 #pragma unroll
-            for (int i = 0; i < EPL; ++i) x[i] = fmul(a.pot.rho, x[i]);
+            for (int i = 0; i < EPL; ++i) rsum[i] = x[i] = fmul(a.pot.rho, x[i]);
             if (opp_slot >= 0) {
               lds_slice<EPL>(tv, stg + opp_slot * LS + l0);
 #pragma unroll
@@ -411,8 +417,10 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
           }
         } else {
 #pragma unroll
+          for (int i = 0; i < EPL; ++i) rsum[i] = 0.0f;
+#pragma unroll
           for (int rr = 0; rr < NRMAX; ++rr) {
-            if (rr < nrows) {
+            if (rr < npl) {
               lds_slice<EPL>(tv, stg + rr * LS + l0);
               const int dd = sd[rr];
               const float rd = xs[4 + 32 * rr + lane];
@@ -421,12 +429,17 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
                 float c = tv[i];
                 if (dd >= 0) {
                   c = fmul(rd, tv[i]);
+                  rsum[i] = fadd(rsum[i], c);
                   if (dd == opp) c = fsub(c, tv[i]);
                 }
                 x[i] = fadd(x[i], c);
               }
             }
           }
+        }
+        if (fuse && !(npl > a0)) {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) rsum[i] = 0.0f;
         }
 
         // ---- decode p: near codes, far targets
@@ -553,6 +566,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         PMARK(4);
         if (!WIN) sts_slice<EPL>(sl + SL::X + l0, x);
         sts_slice<EPL>(sl + SL::B + l0, B);
+        if (fuse) sts_slice<EPL>(sl + SL::DT + l0, rsum);
         if (!BAND) {
           uint8_t* pb = reinterpret_cast<uint8_t*>(sl + SL::P);
 #pragma unroll
@@ -651,6 +665,18 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         }
         __syncwarp();
       };
+      const bool fuse = TRWP && a.dtheta != nullptr;
+      float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
+      float accl[EPL], rhol = 0.0f;  // last step's acc / rho (the head's own contribution)
+      float dtn[EPL];                // dtheta(cur) of the next step, loaded one step ahead
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) accl[i] = 0.0f, dtn[i] = 0.0f;
+      auto load_dt = [&](int s) {
+        const float* src = dthb + o_first + (nsteps - s) * stL + l0;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) dtn[i] = (FULL || i < nvalid) ? __ldcg(src + i) : 0.0f;
+      };
+      if (fuse && nsteps > 0) load_dt(0);
       for (int s = 0; s < nsteps; ++s) {
         const uint32_t gs = gs0 + uint32_t(s);
         const int slot = int(gs % kSplitSlots);
@@ -669,6 +695,15 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         lds_slice<EPL>(gg, sl + SL::X + l0);
         lds_slice<EPL>(cin, sl + SL::CIN + l0);
         stg_slice<EPL>(aout_r + o_first + (j - 1) * stL, l0, acc, nvalid, L);
+        if (fuse) {  // dtheta(cur) += sum_d rho_d A[d](cur) + this sweep's own share (the carry)
+          float dt[EPL], rs[EPL];
+          lds_slice<EPL>(rs, sl + SL::DT + l0);
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) dt[i] = fadd(fadd(dtn[i], rs[i]), cin[i]), accl[i] = acc[i];
+          if (s + 1 < nsteps) load_dt(s + 1);
+          stg_slice<EPL>(dthb + o_first + j * stL, l0, dt, nvalid, L);
+          rhol = __uint_as_float(sc[SC_RHO]);
+        }
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
           gg[i] = fadd(gg[i], cin[i]);
@@ -739,6 +774,32 @@ __global__ void __launch_bounds__(32 * (2 + NPRE)) bwd_split_kernel(AccArgs a) {
         }
         __syncwarp();
         mbar_arrive(bar_empty + slot);
+      }
+      if (fuse) {
+        // the head is no edge's cur: dtheta(head) += sum_{d != 0} rho_d A[d](head) + rho acc_last
+        const int head = ld.first;
+        float hs[EPL], t[EPL];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) hs[i] = 0.0f;
+        for (int d = 1; d < R; ++d) {
+          float rd = a.pot.rho;
+          if (rpl) {
+            const int wn = (d & 1) ? head + g.node_step[d] : head;
+            rd = __ldg(a.pot.rho_planes + (size_t(b) * (R / 2) + (d >> 1)) * N + min(max(wn, 0), N - 1));
+          }
+          const float* src = a.ain + size_t(b) * R * NL + size_t(d) * NL + size_t(head) * L;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) t[i] = (FULL || i < nvalid) ? __ldcg(src + l0 + i) : 0.0f;
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) hs[i] = fadd(hs[i], fmul(rd, t[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          if (FULL || i < nvalid) {
+            float* dst = dthb + size_t(head) * L + l0 + i;
+            *dst = fadd(fadd(*dst, hs[i]), nsteps > 0 ? fmul(rhol, accl[i]) : 0.0f);
+          }
+        }
       }
       if (fkey >= 0) flush_far();
       if (WIN) {

@@ -18,6 +18,9 @@ inline int epl_for(int L) {
   return 8;
 }
 
+// backward kernel choice: one warp per line (L <= 32, many lines) or warp-specialised
+inline bool bwd_uses_small(int L, int nlines, int batch) { return L <= 32 && int64_t(nlines) * batch >= 148 * 16; }
+
 // warps per CTA: few long chains -> spread them over every SM
 inline int warps_per_cta(int nlines) { return nlines >= 148 * 8 ? 4 : (nlines >= 148 * 2 ? 2 : 1); }
 

@@ -353,22 +353,31 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
     float* ain = TRWP ? A[0] : A[(k + 1) & 1];
     float* aout = TRWP ? A[0] : A[k & 1];
     if (TRWP) {
+      // the warp-specialised kernel's last sweep of the iteration also collects
+      // the iteration's unary gradient; the one-warp-per-line kernel leaves it
+      // to dtheta_acc_kernel
+      const bool fuse = !bwd_uses_small(L, int(topo->dir_lines_all[0].size()), B);
       for (int r = R - 1; r >= 0; --r) {  // directions in reverse (autodiff.hpp:147)
         AccArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), p, q, k, grad_cost,
-                  ain, aout, grads->weight_planes, gvacc, desc.get()};
+                  ain, aout, grads->weight_planes, gvacc, desc.get(), (r == 0 && fuse) ? grads->unary : nullptr};
         ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         cuda_check(launch_bwd_trwp(a, B, stream), "bwd_split_kernel launch");
       }
+      if (!fuse) {
+        ProfScope ps(stream, MRF_KCLASS_AUX);
+        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary);
+        cuda_check(cudaGetLastError(), "dtheta_acc launch");
+      }
     } else {
-      AccArgs a{g, pot, lines + topo->every_start, int(topo->every_line.size()), p, q, k, grad_cost,
-                ain, aout, isgmr_dw ? dwr : nullptr, gvacc, desc.get()};
-      ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
-      cuda_check(launch_bwd_isgmr(a, B, stream), "bwd_split_kernel launch");
-    }
-    {
+      {
+        AccArgs a{g, pot, lines + topo->every_start, int(topo->every_line.size()), p, q, k, grad_cost,
+                  ain, aout, isgmr_dw ? dwr : nullptr, gvacc, desc.get(), nullptr};
+        ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
+        cuda_check(launch_bwd_isgmr(a, B, stream), "bwd_split_kernel launch");
+      }
+      // ISGMR's directions run concurrently: the unary gradient is collected after the launch
       ProfScope ps(stream, MRF_KCLASS_AUX);
-      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, TRWP ? pr->rho_planes : nullptr, g,
-                                                           grads->unary);
+      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary);
       cuda_check(cudaGetLastError(), "dtheta_acc launch");
     }
   }
