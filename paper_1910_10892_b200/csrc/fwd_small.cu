@@ -1,0 +1,39 @@
+// Instantiations of the small-L dense forward (L <= 32; 4 / 8 directions).
+#include "fwd_small.cuh"
+#include "launch.hpp"
+
+namespace mrf {
+
+template <bool TRWP, int R, int LMAX, bool WPL>
+static cudaError_t run1(const FwdArgs& a, int batch, cudaStream_t s) {
+  constexpr int rows = 1 + (TRWP ? R - 1 : R - 2);
+  const int wpc = 4;
+  const int smem = kStages * fwd_small_stage(rows) * int(sizeof(float)) * wpc;
+  auto kern = fwd_small_kernel<TRWP, R, LMAX, WPL>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <bool TRWP, int R, int LMAX>
+static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
+  return a.pot.w_planes ? run1<TRWP, R, LMAX, true>(a, batch, s) : run1<TRWP, R, LMAX, false>(a, batch, s);
+}
+
+template <bool TRWP, int R>
+static cudaError_t run_l(const FwdArgs& a, int batch, cudaStream_t s) {
+  if (a.g.L <= 8) return run<TRWP, R, 8>(a, batch, s);
+  if (a.g.L <= 16) return run<TRWP, R, 16>(a, batch, s);
+  if (a.g.L <= 24) return run<TRWP, R, 24>(a, batch, s);
+  return run<TRWP, R, 32>(a, batch, s);
+}
+
+bool fwd_small_applies(int L, int R) { return L <= 32 && (R == 4 || R == 8); }
+cudaError_t launch_fwd_small(const FwdArgs& a, int batch, bool trwp, cudaStream_t s) {
+  if (a.g.R == 4) return trwp ? run_l<true, 4>(a, batch, s) : run_l<false, 4>(a, batch, s);
+  return trwp ? run_l<true, 8>(a, batch, s) : run_l<false, 8>(a, batch, s);
+}
+
+}  // namespace mrf

@@ -1,0 +1,152 @@
+// Forward sweep for small label sets with a dense (explicit) V, L <= 32
+// (the segmentation config: 21 labels, learned 21x21 V, per-edge weights,
+// batch 32), one warp per scanline, lane = label (sm_100a). The reference's
+// min-plus (isgmr.hpp:98-131 / trwp.hpp:100-133) as written: for every
+// label l the candidates mu = 0..L-1 in ascending order with strict '<',
+// cost fl(base(mu) + fl(w V'(mu, l))) -- base(mu) comes from lane mu by a
+// shuffle, V'(., l) is the lane's column of V (orientation r & 1) held in
+// registers for the line, pre-multiplied by w once per line when w is
+// constant. Then the reparametrisation's first argmin (-0 carried as in the
+// reference) and m = out - min.
+#pragma once
+
+#include "fwd_warp.cuh"
+
+namespace mrf {
+
+// per-warp ring stage: ROWS rows of 32 floats + {w, rho}
+__host__ __device__ constexpr int fwd_small_stage(int rows) { return rows * 32 + 2; }
+
+template <bool TRWP, int R, int LMAX, bool WPL>
+__global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
+  if (a.desc->banded || WPL != (a.pot.w_planes != nullptr)) return;  // another kernel owns the sweep
+  extern __shared__ float smem[];
+  constexpr int NP = TRWP ? R - 1 : R - 2;
+  constexpr int ROWS = NP + 1;
+  constexpr int STG = fwd_small_stage(ROWS);
+  const Geometry& g = a.g;
+  const int L = g.L, N = g.N;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
+  float* ring = smem + size_t(wid) * kStages * STG;
+  const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+  const int b = blockIdx.y;
+  const bool valid = lane < L;
+  const float* un = a.pot.unary + size_t(b) * N * L + lane;
+  const size_t img = size_t(b) * R * N * L;
+  constexpr bool wpl = WPL;
+  const bool rpl = TRWP && a.pot.rho_planes != nullptr;
+  const int l = valid ? lane : 0;
+  int v_orient = -1;
+  float vcol[LMAX], wv[LMAX];
+
+  for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
+    const LineDesc ld = a.lines[li];
+    const int r = ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
+    const int nsteps = ld.length - 1;
+    if (v_orient != (r & 1)) {  // V'(mu, l) = V(mu, l) (even r) / V(l, mu) (odd r)
+      v_orient = r & 1;
+#pragma unroll
+      for (int mu = 0; mu < LMAX; ++mu)
+        vcol[mu] = mu < L ? __ldg(a.pot.V + (v_orient ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+#pragma unroll
+      for (int mu = 0; mu < LMAX; ++mu) wv[mu] = wpl ? 0.0f : fmul(a.pot.w, vcol[mu]);
+    }
+    const float* rowp[ROWS];
+    rowp[0] = un;
+#pragma unroll
+    for (int rr = 1; rr < ROWS; ++rr) {
+      const int idx = rr - 1;
+      const int d = TRWP ? (idx < r ? idx : idx + 1) : (idx < (r & ~1) ? idx : idx + 2);
+      rowp[rr] = a.m_in + img + size_t(d) * N * L + lane;
+    }
+    const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
+    const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
+    auto issue = [&](int j) {
+      const uint32_t base_s = ring_s + 4u * uint32_t(((j - 1) % kStages) * STG);
+      const int prev = ld.first + (j - 1) * st;
+      if (valid) {
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr) cp_async_u32(base_s + 4u * (rr * 32 + lane), rowp[rr] + size_t(prev) * L, 4);
+      }
+      const int wnode = (r & 1) ? prev + st : prev;
+      if (wpl && lane == 0) cp_async_u32(base_s + 4u * (ROWS * 32), wrow + wnode, 4);
+      if (rpl && lane == 1) cp_async_u32(base_s + 4u * (ROWS * 32 + 1), rrow + wnode, 4);
+    };
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+      if (1 + s <= nsteps) issue(1 + s);
+      cp_commit();
+    }
+    const size_t pq_base = (size_t(b) * g.K_cap + a.k) * g.E + g.dir_offset[r] + ld.edge_base;
+    float* mout = a.m_out + img + size_t(r) * N * L + lane;
+    float carry = 0.0f;
+
+    for (int j = 1; j <= nsteps; ++j) {
+      if (j + kStages - 1 <= nsteps) issue(j + kStages - 1);
+      cp_commit();
+      cp_wait<kStages - 1>();
+      __syncwarp();  // the edge scalars were copied by lanes 0 / 1
+      const float* srow = ring + ((j - 1) % kStages) * STG + lane;
+      // ---- base (isgmr.hpp:82-88 / trwp.hpp:84-90 addition order)
+      float base;
+      if (!TRWP) {
+        base = fadd(srow[0], carry);
+#pragma unroll
+        for (int rr = 1; rr < ROWS; ++rr) base = fadd(base, srow[rr * 32]);
+      } else {
+        const float rho = rpl ? srow[ROWS * 32 + 1 - lane] : a.pot.rho;
+        float s = srow[0], mo = 0.0f;
+#pragma unroll
+        for (int d = 0; d < R; ++d) {
+          const float t = srow[(d < r ? d + 1 : (d > r ? d : 1)) * 32];
+          mo = d == opp ? t : mo;
+          s = fadd(s, d == r ? carry : t);
+        }
+        base = fsub(fmul(rho, s), mo);
+      }
+      const float w = wpl ? srow[ROWS * 32 - lane] : 0.0f;
+      if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
+      // ---- dense min-plus, ascending mu, strict '<': independent chains over
+      // mu blocks of 8 (shorter dependency chains), merged in index order with
+      // the earlier block winning ties
+      constexpr int NB = LMAX / 8;
+      float bb[NB];
+      int ba[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) bb[c] = kInf, ba[c] = 0;
+#pragma unroll
+      for (int mu = 0; mu < LMAX; ++mu) {
+        const float bm = __shfl_sync(0xffffffffu, base, mu);
+        const int c = mu / 8;
+        const float v = fadd(bm, wpl ? fmul(w, vcol[mu]) : wv[mu]);
+        const bool p = v < bb[c];
+        bb[c] = p ? v : bb[c];
+        ba[c] = p ? mu : ba[c];
+      }
+      float best = bb[0];
+      int arg = ba[0];
+#pragma unroll
+      for (int c = 1; c < NB; ++c) {
+        const bool p = bb[c] < best;
+        best = p ? bb[c] : best;
+        arg = p ? ba[c] : arg;
+      }
+      // ---- p, reparametrisation first argmin (lowest label, -0 as the reference)
+      if (valid) a.p[(pq_base + j - 1) * L + lane] = uint8_t(arg);
+      const uint32_t lk = valid ? order_key(fadd(best, 0.0f)) : 0xffffffffu;
+      const uint32_t lt = valid ? (uint32_t(lane) << 1) | (__float_as_uint(best) == 0x80000000u ? 1u : 0u) : 0xffffffffu;
+      const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
+      const uint32_t tmin = __reduce_min_sync(0xffffffffu, lk == kmin ? lt : 0xffffffffu);
+      float lo = key_value(kmin);
+      if (tmin & 1u) lo = -0.0f;
+      carry = fsub(best, lo);
+      const int cur = ld.first + j * st;
+      if (valid) mout[size_t(cur) * L] = carry;
+      if (lane == 0) a.q[pq_base + j - 1] = uint8_t(tmin >> 1);
+    }
+    cp_wait<0>();
+    __syncwarp();
+  }
+}
+
+}  // namespace mrf

@@ -81,6 +81,7 @@ struct FwdArgs {
   const PairDesc* desc;
   int band2_launched;  // fwd_band2_kernel covers banded D == 2 in this sweep
   int bandw_max;       // fwd_bandw_kernel covers banded 2 < D <= bandw_max (0: not launched)
+  int dense_small;     // fwd_small_kernel covers dense V with L <= 32
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(128) fwd_warp_kernel(FwdArgs a) {
     } else if (!(a.desc->D > 2 && a.desc->D <= a.bandw_max)) {
       fwd_sweep_lines<EPL, TRWP, 1>(a, ws);
     }
-  } else {
+  } else if (!a.dense_small) {
     fwd_sweep_lines<EPL, TRWP, 0>(a, ws);
   }
 }

@@ -31,6 +31,8 @@ cudaError_t ensure_dynamic_smem(const void* kern, int bytes);
 cudaError_t launch_fwd_generic(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 cudaError_t launch_fwd_bandw(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 int fwd_bandw_max();  // widest band D the wide-band forward covers
+bool fwd_small_applies(int L, int R);  // dense small-L forward (fwd_small.cuh) covers the sweep
+cudaError_t launch_fwd_small(const FwdArgs& a, int batch, bool trwp, cudaStream_t s);
 cudaError_t launch_fwd_band2_isgmr(const FwdArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_fwd_band2_trwp(const FwdArgs& a, int batch, cudaStream_t s);
 cudaError_t launch_bwd_isgmr(const AccArgs& a, int batch, cudaStream_t s);

@@ -268,13 +268,16 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
   // D == 2 specialisation and the generic kernel are both launched; each
   // returns at once when the other one owns the sweep.
   const bool band2 = g.R == 4 || g.R == 8;
-  FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0, band2 ? fwd_bandw_max() : 0};
+  const bool small = fwd_small_applies(g.L, g.R);
+  FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0, band2 ? fwd_bandw_max() : 0,
+            small ? 1 : 0};
   ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
   if (band2) {
     cuda_check(TRWP ? launch_fwd_band2_trwp(a, pr->batch, stream) : launch_fwd_band2_isgmr(a, pr->batch, stream),
                "fwd_band2_kernel launch");
     cuda_check(launch_fwd_bandw(a, pr->batch, TRWP, stream), "fwd_bandw_kernel launch");
   }
+  if (small) cuda_check(launch_fwd_small(a, pr->batch, TRWP, stream), "fwd_small_kernel launch");
   cuda_check(launch_fwd_generic(a, pr->batch, TRWP, stream), "fwd_warp_kernel launch");
 }
 
