@@ -38,22 +38,33 @@ struct PairDesc {
 // One block. Bit-level checks: symmetric Toeplitz, constant tail, and no -0
 // in the constant weight (planes are checked by scan_neg_zero_kernel), so no
 // candidate value can be -0, which makes the scanned minimum value equal to
-// the first argmin's raw value.
-static __global__ void analyze_pairwise_kernel(const float* __restrict__ V, int L, float wconst, int has_wplanes,
-                                               PairDesc* __restrict__ out) {
+// the first argmin's raw value. D = 1 + the last index d < L-1 whose g(d)
+// differs from the tail g(L-1) (at least 1), found by a block max-reduction.
+static __global__ void __launch_bounds__(1024) analyze_pairwise_kernel(const float* __restrict__ V, int L, float wconst,
+                                                                       int has_wplanes, PairDesc* __restrict__ out) {
   int ok = 1;
   for (int i = threadIdx.x; i < L * L; i += blockDim.x) {
     const int a = i / L, b = i - a * L;
     const int d = a > b ? a - b : b - a;
-    if (__float_as_uint(V[i]) != __float_as_uint(V[d])) ok = 0;
+    if (__float_as_uint(__ldg(V + i)) != __float_as_uint(__ldg(V + d))) ok = 0;
   }
   if (!has_wplanes && __float_as_uint(wconst) == 0x80000000u) ok = 0;
   ok = __syncthreads_and(ok);
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) out->g[d] = d < L ? V[d] : 0.0f;
+  const uint32_t tail = __float_as_uint(V[L - 1]);
+  int last = 0;  // 1 + the last d < L-1 with g(d) != g(L-1)
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    const float gd = d < L ? V[d] : 0.0f;
+    out->g[d] = gd;
+    if (d < L - 1 && __float_as_uint(gd) != tail) last = d + 1;
+  }
+  __shared__ int s_last[32];
+  for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(0xffffffffu, last, o));
+  if ((threadIdx.x & 31) == 0) s_last[threadIdx.x >> 5] = last;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int D = L > 1 ? L - 1 : 1;
-    const uint32_t tail = __float_as_uint(V[L - 1]);
-    while (D > 1 && __float_as_uint(V[D - 1]) == tail) --D;
+    int m = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) m = max(m, s_last[w]);
+    const int D = L > 1 ? max(m, 1) : 1;
     out->D = D;
     out->banded = ok && (2 * D - 1) * 2 <= L;
   }

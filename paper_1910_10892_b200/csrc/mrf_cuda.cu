@@ -242,7 +242,7 @@ class PairDescHolder {
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_), sizeof(PairDesc), s), "cudaMallocAsync(desc)");
     const int64_t planes = int64_t(pr->batch) * (R / 2) * pr->height * pr->width;
     ProfScope ps(s, MRF_KCLASS_AUX);
-    analyze_pairwise_kernel<<<1, 256, 0, s>>>(pr->pairwise, pr->labels, pr->weight, pr->weight_planes != nullptr, d_);
+    analyze_pairwise_kernel<<<1, 1024, 0, s>>>(pr->pairwise, pr->labels, pr->weight, pr->weight_planes != nullptr, d_);
     cuda_check(cudaGetLastError(), "analyze_pairwise launch");
     for (const float* pl : {pr->weight_planes, pr->rho_planes}) {
       if (!pl) continue;
