@@ -168,6 +168,26 @@ int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const m
  * per training step, over the buffer mrf_pack_shared_grads_f32 produced. */
 int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream);
 
+/* ------------------------------------------------- readout and evaluation */
+
+/* Replaces mp::soft_head_forward<float> + mp::soft_head_backward<float>
+ * (softhead.hpp:22-74) for a batch, fused in one pass over the cost volume:
+ * per node confidence = softmax(-c), disparity d = sum_l l f_l, loss[b] =
+ * mean_i |d_i - target_i| (device float [B], accumulated in double), and
+ * grad_cost = d loss / d c = sign(d - t)/N * (-f (l - d)) (zero on exact
+ * ties). cost [B][N][L], target [B][N]; confidence [B][N][L], disparity
+ * [B][N] and grad_cost [B][N][L] may be NULL. Stream-ordered. */
+int mrf_soft_head_f32(int batch, int nodes, int labels, const float* cost, const float* target, float* confidence,
+                      float* disparity, float* grad_cost, float* loss, cudaStream_t stream);
+
+/* Replaces mp::energy<float, uint16_t> (potentials.hpp:175-199): unaries plus
+ * every undirected edge once (the even direction of each family), in double,
+ * for each image of the batch. labels [B][N] (device), energy: host double
+ * [B]. Synchronises `stream`; MRF_EINVAL when a label is out of range (the
+ * reference's std::out_of_range). */
+int mrf_energy_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const uint16_t* labels, double* energy,
+                   cudaStream_t stream);
+
 /* ---------------------------------------------------------- instrumentation */
 
 /* Kernel classes for the launch profiler. */

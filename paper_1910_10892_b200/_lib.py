@@ -64,6 +64,8 @@ SIGNATURES = {
     "mrf_trwp_backward_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _GR, _vp, _sz, _vp]),
     "mrf_pack_shared_grads_f32": (_i, [_PP, _i, _GR, _vp, _vp]),
     "mrf_allreduce_grads_f32": (_i, [_vp, _vp, _sz, _vp]),
+    "mrf_soft_head_f32": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "mrf_energy_f32": (_i, [_vp, _PP, _vp, C.POINTER(C.c_double), _vp]),
     "mrf_profiler_enable": (_i, [_i]),
     "mrf_profiler_read": (_i, [_i, C.POINTER(C.c_double), _i64p]),
 }

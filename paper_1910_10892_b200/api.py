@@ -334,3 +334,75 @@ def pack_shared_grads(mrf: MRF, grads: GradientSet, out=None, stream=None):
     g = _lib.Grads(_ptr(grads.unary), _ptr(grads.pairwise), _ptr(grads.edge_weights))
     check(lib().mrf_pack_shared_grads_f32(C.byref(pr), mrf.topo.num_dirs, C.byref(g), _ptr(out), _stream(stream)))
     return out
+
+
+# ------------------------------------------------------------------ readout and evaluation
+
+@dataclass
+class SoftHeadResult:
+    """mp::SoftHeadResult (softhead.hpp:15-20), batched; grad_cost is the
+    soft_head_backward output (softhead.hpp:58-74), produced in the same pass."""
+    confidence: torch.Tensor | None  # [B, N, L]
+    disparity: torch.Tensor          # [B, N]
+    loss: torch.Tensor               # [B] mean |disparity - target|
+    grad_cost: torch.Tensor | None   # [B, N, L] d loss / d cost
+
+
+def soft_head(cost: torch.Tensor, target: torch.Tensor, confidence: bool = False, grad: bool = True,
+              stream=None) -> SoftHeadResult:
+    """soft_head_forward + soft_head_backward (softhead.hpp:22-74) fused:
+    cost [B, N, L] (aggregate output), target [B, N]."""
+    if cost.dim() == 2:
+        cost = cost.unsqueeze(0)
+    if target.dim() == 1:
+        target = target.unsqueeze(0)
+    B, N, L = cost.shape
+    if tuple(target.shape) != (B, N):
+        raise _lib.MrfInvalidArgument(1, "soft_head_forward: target size mismatch")
+    cost, target = cost.contiguous(), target.contiguous()
+    conf = torch.empty_like(cost) if confidence else None
+    disp = torch.empty((B, N), dtype=torch.float32, device=cost.device)
+    g = torch.empty_like(cost) if grad else None
+    loss = torch.empty(B, dtype=torch.float32, device=cost.device)
+    check(lib().mrf_soft_head_f32(B, N, L, _ptr(cost), _ptr(target), _ptr(conf) if conf is not None else None,
+                                  _ptr(disp), _ptr(g) if g is not None else None, _ptr(loss), _stream(stream)))
+    return SoftHeadResult(conf, disp, loss, g)
+
+
+def energy(mrf: MRF, labels: torch.Tensor, topo: GridTopology | None = None, stream=None):
+    """mp::energy (potentials.hpp:175-199) of a labelling per image (float64
+    numpy [B]); `topo` may be a separate evaluation topology of the same grid
+    (the 4-connected protocol, mrfmp.cpp:91-94)."""
+    t = topo or mrf.topo
+    if labels.dim() == 1:
+        labels = labels.unsqueeze(0)
+    labels = labels.contiguous()
+    if labels.dtype not in (torch.int16, torch.uint16) or tuple(labels.shape) != (mrf.batch, t.nodes):
+        raise _lib.MrfInvalidArgument(1, "energy: labelling size mismatch")
+    m = mrf
+    if t is not mrf.topo:
+        if (t.height, t.width) != (mrf.topo.height, mrf.topo.width) or t.num_dirs > mrf.topo.num_dirs:
+            raise _lib.MrfInvalidArgument(1, "energy: evaluation topology must be the same grid with <= directions")
+        w = mrf.weight
+        if isinstance(w, torch.Tensor):  # families of the evaluation directions (same order)
+            w = w[:, : t.num_dirs // 2].contiguous()
+        m = MRF(t, mrf.unary, mrf.V, w, 0.5)
+    pr = m.c_problem()
+    out = (C.c_double * mrf.batch)()
+    check(lib().mrf_energy_f32(t.handle, C.byref(pr), _ptr(labels), out, _stream(stream)))
+    import numpy as np
+
+    return np.array(out[:], dtype=np.float64)
+
+
+def iterate_energy(engine: str, mrf: MRF, iterations: int, eval_topo: GridTopology | None = None, stream=None):
+    """isgmr_iterate_energy / trwp_iterate_energy (isgmr.hpp:156-169,
+    trwp.hpp:158-171): energy of the aggregated labelling after each
+    iteration, on eval_topo when given."""
+    eng = (IsgmrEngine if engine == "isgmr" else TrwpEngine)(mrf, iterations)
+    out = []
+    for _ in range(iterations):
+        eng.step(stream)
+        _, labels = eng.aggregate(stream)
+        out.append(energy(mrf, labels, eval_topo, stream))
+    return out

@@ -18,6 +18,18 @@ inline int epl_for(int L) {
   return 8;
 }
 
+// Readout and evaluation (head.cu)
+struct EvenSteps {
+  int dh[8], dw[8];  // step of direction 2f (the even direction of family f)
+};
+cudaError_t launch_soft_head(int B, int N, int L, const float* cost, const float* target, float* conf, float* disp,
+                             float* grad, float* loss, double* partial, int nblk, cudaStream_t s);
+int soft_head_blocks(int N);
+cudaError_t launch_energy(int B, int H, int W, int L, int R, const EvenSteps& st, const float* unary, const float* V,
+                          float w, const float* wplanes, const uint16_t* labels, double* out, double* partial, int nblk,
+                          int* bad, cudaStream_t s);
+int energy_blocks(int N);
+
 // backward kernel choice: one warp per line (L <= 32, many lines) or warp-specialised
 inline bool bwd_uses_small(int L, int nlines, int batch) { return L <= 32 && int64_t(nlines) * batch >= 148 * 16; }
 

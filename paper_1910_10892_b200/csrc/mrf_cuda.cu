@@ -561,6 +561,55 @@ int mrf_trwp_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
   });
 }
 
+int mrf_soft_head_f32(int batch, int nodes, int labels, const float* cost, const float* target, float* confidence,
+                      float* disparity, float* grad_cost, float* loss, cudaStream_t stream) {
+  return guarded([&] {
+    if (batch < 1 || nodes < 1 || labels < 1) fail(MRF_EINVAL, "soft_head: empty volume");
+    if (!cost || !target || !loss) fail(MRF_EINVAL, "soft_head: null cost, target or loss");
+    const int nblk = soft_head_blocks(nodes);
+    double* partial = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&partial), sizeof(double) * batch * nblk, stream),
+               "cudaMallocAsync(soft head partials)");
+    ProfScope ps(stream, MRF_KCLASS_AUX);
+    cuda_check(launch_soft_head(batch, nodes, labels, cost, target, confidence, disparity, grad_cost, loss, partial,
+                                nblk, stream),
+               "soft_head launch");
+    cuda_check(cudaFreeAsync(partial, stream), "cudaFreeAsync");
+  });
+}
+
+int mrf_energy_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const uint16_t* labels, double* energy,
+                   cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (!labels || !energy) fail(MRF_EINVAL, "energy: null labels or output");
+    const int B = prob->batch, H = topo->host.height(), W = topo->host.width(), R = topo->host.num_dirs();
+    EvenSteps st{};
+    for (int r = 0; r < R; r += 2) st.dh[r >> 1] = direction_step(r).dh, st.dw[r >> 1] = direction_step(r).dw;
+    const int nblk = energy_blocks(H * W);
+    double* partial = nullptr;
+    double* out = nullptr;
+    int* bad = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&partial), sizeof(double) * (size_t(B) * nblk + B) + 16, stream),
+               "cudaMallocAsync(energy)");
+    out = partial + size_t(B) * nblk;
+    bad = reinterpret_cast<int*>(out + B);
+    cuda_check(cudaMemsetAsync(bad, 0, sizeof(int), stream), "zero flag");
+    {
+      ProfScope ps(stream, MRF_KCLASS_AUX);
+      cuda_check(launch_energy(B, H, W, prob->labels, R, st, prob->unary, prob->pairwise, prob->weight,
+                               prob->weight_planes, labels, out, partial, nblk, bad, stream),
+                 "energy launch");
+    }
+    int hbad = 0;
+    cuda_check(cudaMemcpyAsync(energy, out, sizeof(double) * B, cudaMemcpyDeviceToHost, stream), "energy D2H");
+    cuda_check(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, stream), "flag D2H");
+    cuda_check(cudaFreeAsync(partial, stream), "cudaFreeAsync");
+    cuda_check(cudaStreamSynchronize(stream), "energy sync");
+    if (hbad) fail(MRF_EINVAL, "energy: label out of range");
+  });
+}
+
 int mrf_profiler_enable(int on) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_prof.mu);
