@@ -572,4 +572,82 @@ GradientSet<Real> trwp_backward(const GridTopology& topo, const PotentialSet<Rea
   return cuda_detail::backward(MRF_ENGINE_TRWP, topo, pots, &rho, indices, grad_cost);
 }
 
+/// softhead.hpp:15-20
+template <class Real>
+struct SoftHeadResult {
+  std::vector<Real> confidence;  // N*L, softmax(-c) per node
+  std::vector<Real> disparity;   // N, expected label under confidence
+  Real loss;                     // mean absolute error against ground truth
+};
+
+namespace cuda_detail {
+
+// One fused pass (mrf_soft_head_f32): confidence, disparity, loss and, when
+// grad != nullptr, the loss gradient with respect to the cost volume.
+inline SoftHeadResult<float> soft_head(const CostOutput<float>& cost, const std::vector<float>& target,
+                                       std::vector<float>* grad, const char* who) {
+  const int L = cost.labels;
+  const size_t n = L ? cost.cost.size() / size_t(L) : 0;
+  if (target.size() != n) throw std::invalid_argument(std::string(who) + ": target size mismatch");
+  SoftHeadResult<float> res;
+  res.confidence.resize(cost.cost.size());
+  res.disparity.resize(n);
+  res.loss = 0.0f;
+  if (n == 0) return res;
+  auto c = DeviceBuffer::upload(cost.cost.data(), cost.cost.size());
+  auto t = DeviceBuffer::upload(target.data(), target.size());
+  DeviceBuffer f(sizeof(float) * cost.cost.size()), d(sizeof(float) * n), g(grad ? sizeof(float) * cost.cost.size() : 0),
+      loss(sizeof(float));
+  check(mrf_soft_head_f32(1, int(n), L, c.as<float>(), t.as<float>(), f.as<float>(), d.as<float>(),
+                          grad ? g.as<float>() : nullptr, loss.as<float>(), nullptr));
+  f.download(res.confidence.data(), res.confidence.size());
+  d.download(res.disparity.data(), n);
+  loss.download(&res.loss, 1);
+  if (grad) {
+    grad->resize(cost.cost.size());
+    g.download(grad->data(), grad->size());
+  }
+  return res;
+}
+
+}  // namespace cuda_detail
+
+/// softhead.hpp:22-56
+template <class Real>
+SoftHeadResult<Real> soft_head_forward(const CostOutput<Real>& cost, const std::vector<Real>& target) {
+  cuda_detail::require_float<Real>();
+  return cuda_detail::soft_head(cost, target, nullptr, "soft_head_forward");
+}
+
+/// softhead.hpp:58-74 (the gradient is recomputed from the cost volume in the
+/// same fused pass; `head` is the forward's result for the same inputs)
+template <class Real>
+std::vector<Real> soft_head_backward(const CostOutput<Real>& cost, const SoftHeadResult<Real>& head,
+                                     const std::vector<Real>& target) {
+  cuda_detail::require_float<Real>();
+  (void)head;
+  std::vector<float> grad;
+  cuda_detail::soft_head(cost, target, &grad, "soft_head_backward");
+  return grad;
+}
+
+/// potentials.hpp:175-199
+template <class Real, class Label>
+double energy(const GridTopology& topo, const PotentialSet<Real>& pots, const std::vector<Label>& labels) {
+  cuda_detail::require_float<Real>();
+  const GridGraph& g = topo.grid();
+  if (static_cast<int>(labels.size()) != g.nodes()) throw std::invalid_argument("energy: labelling size mismatch");
+  std::vector<std::uint16_t> lab(labels.size());
+  for (size_t i = 0; i < labels.size(); ++i) {
+    const long long x = static_cast<long long>(labels[i]);
+    if (x < 0 || x >= pots.unary.labels) throw std::out_of_range("energy: label out of range");
+    lab[i] = static_cast<std::uint16_t>(x);
+  }
+  auto d = cuda_detail::upload(topo, pots, nullptr, false);
+  auto dl = cuda_detail::DeviceBuffer::upload(lab.data(), lab.size());
+  double e = 0.0;
+  cuda_detail::check(mrf_energy_f32(topo.handle(), &d.prob, dl.as<std::uint16_t>(), &e, nullptr));
+  return e;
+}
+
 }  // namespace mp

@@ -115,6 +115,48 @@ int main() {
     threw = true;
   }
   CHECK(threw);
+  // readout and evaluation (softhead.hpp:22-74, potentials.hpp:175-199)
+  {
+    const int H = 6, W = 7, L = 9;
+    std::mt19937 rng(7);
+    std::uniform_real_distribution<float> U(0.f, 8.f);
+    CostOutput<float> c;
+    c.height = H, c.width = W, c.labels = L;
+    c.cost.resize(size_t(H) * W * L);
+    for (auto& v : c.cost) v = U(rng);
+    std::vector<float> target(size_t(H) * W);
+    for (auto& v : target) v = U(rng);
+    const auto head = soft_head_forward(c, target);
+    const auto grad = soft_head_backward(c, head, target);
+    std::vector<float> d_ref(target.size()), g_ref(c.cost.size());
+    const float loss_ref = orc_soft_head(H * W, L, c.cost.data(), target.data(), d_ref.data(), g_ref.data());
+    CHECK(std::fabs(head.loss - loss_ref) <= 1e-5f * std::fabs(loss_ref));
+    CHECK(normwise(head.disparity, d_ref) <= 1e-5);
+    CHECK(normwise(grad, g_ref) <= 1e-5);
+    PotentialSet<float> pots;
+    pots.unary = UnaryVolume<float>(H, W, L);
+    for (auto& v : pots.unary.values) v = U(rng);
+    pots.pairwise = build_pairwise<float>(PairwiseKind::potts, {}, L);
+    const GridTopology t4(GridGraph(H, W), DirectionSet::build(4));
+    std::vector<std::uint16_t> lab(size_t(H) * W);
+    for (auto& x : lab) x = std::uint16_t(rng() % L);
+    double want = 0.0;
+    for (int i = 0; i < H * W; ++i) want += double(pots.unary.values[size_t(i) * L + lab[i]]);
+    for (int h = 0; h < H; ++h)
+      for (int w = 0; w < W; ++w) {
+        if (w + 1 < W) want += (lab[h * W + w] != lab[h * W + w + 1]) ? 1.0 : 0.0;
+        if (h + 1 < H) want += (lab[h * W + w] != lab[(h + 1) * W + w]) ? 1.0 : 0.0;
+      }
+    CHECK(std::fabs(energy(t4, pots, lab) - want) <= 1e-9 * std::fabs(want));
+    lab[3] = std::uint16_t(L);
+    bool oor = false;
+    try {
+      energy(t4, pots, lab);
+    } catch (const std::out_of_range&) {
+      oor = true;
+    }
+    CHECK(oor);
+  }
   std::printf(failures ? "host_api_test: %d FAILURES\n" : "host_api_test: OK%.0d\n", failures);
   return failures ? 1 : 0;
 }
