@@ -188,6 +188,14 @@ int mrf_soft_head_f32(int batch, int nodes, int labels, const float* cost, const
 int mrf_energy_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const uint16_t* labels, double* energy,
                    cudaStream_t stream);
 
+/* Replaces mp::sgm_forward<float>(topo, pots, variant, threads)
+ * (baselines.hpp:31-98). variant 0 = SgmVariant::standard (the message keeps
+ * the unary; cost = sum_r m^r), 1 = SgmVariant::revised (== one ISGMR
+ * iteration, test_baselines.cpp:58-68). messages [B][R][N][L] (required),
+ * cost [B][N][L] and labels [B][N] (may be NULL). Stream-ordered. */
+int mrf_sgm_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int variant, float* messages, float* cost,
+                uint16_t* labels, cudaStream_t stream);
+
 /* ---------------------------------------------------------- instrumentation */
 
 /* Kernel classes for the launch profiler. */

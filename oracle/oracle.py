@@ -99,6 +99,7 @@ def _ref():
         lib.ref_soft_head_f32.argtypes = [C.c_int] * 3 + [_vp] * 5
         lib.ref_sgm_revised_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp]
         lib.ref_energy_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp]
+        lib.ref_sgm_standard_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp, _vp]
         lib.ref_gradient_check.argtypes = [C.c_int] * 7 + [C.c_uint64, _vp, _vp, _vp]
         lib._typed = True
     return lib
@@ -307,6 +308,15 @@ def ref_sgm_revised(pr: Problem):
     _check_ref(_ref().ref_sgm_revised_f32(pr.H, pr.W, pr.L, pr.conn, _ptr(pr.unary), _ptr(pr.V), pr.w_const,
                                           _ptr(pr.w_planes), _ptr(cost), _ptr(msg)))
     return cost, msg
+
+
+def ref_sgm_standard(pr: Problem):
+    cost = np.zeros(pr.N * pr.L, np.float32)
+    labels = np.zeros(pr.N, np.uint16)
+    msg = np.zeros(pr.conn * pr.N * pr.L, np.float32)
+    _check_ref(_ref().ref_sgm_standard_f32(pr.H, pr.W, pr.L, pr.conn, _ptr(pr.unary), _ptr(pr.V), pr.w_const,
+                                           _ptr(pr.w_planes), _ptr(cost), _ptr(labels), _ptr(msg)))
+    return cost, labels, msg
 
 
 def ref_energy(pr: Problem, labels) -> float:

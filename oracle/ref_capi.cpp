@@ -236,6 +236,19 @@ REF_API int ref_sgm_revised_f32(int H, int W, int L, int conn, const float* unar
   });
 }
 
+/// Standard SGM (baselines.hpp:31-98, SgmVariant::standard): cost, labels, messages.
+REF_API int ref_sgm_standard_f32(int H, int W, int L, int conn, const float* unary, const float* table,
+                                 float w_const, const float* w_planes, float* cost, uint16_t* labels, float* messages) {
+  return guarded([&] {
+    const auto topo = make_topo(H, W, conn);
+    const auto pots = make_pots<float>(H, W, L, conn, unary, table, w_const, w_planes);
+    const auto res = mp::sgm_forward(topo, pots, mp::SgmVariant::standard, 1);
+    if (cost) std::memcpy(cost, res.output.cost.data(), sizeof(float) * res.output.cost.size());
+    if (labels) std::memcpy(labels, res.output.labels_map.data(), sizeof(uint16_t) * res.output.labels_map.size());
+    if (messages) std::memcpy(messages, res.messages.data(), sizeof(float) * res.messages.size());
+  });
+}
+
 /// Energy of a labelling (potentials.hpp:175-199), double accumulation.
 REF_API int ref_energy_f32(int H, int W, int L, int conn, const float* unary, const float* table,
                            float w_const, const float* w_planes, const uint16_t* labels, double* out) {

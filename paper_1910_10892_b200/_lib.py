@@ -66,6 +66,7 @@ SIGNATURES = {
     "mrf_allreduce_grads_f32": (_i, [_vp, _vp, _sz, _vp]),
     "mrf_soft_head_f32": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mrf_energy_f32": (_i, [_vp, _PP, _vp, C.POINTER(C.c_double), _vp]),
+    "mrf_sgm_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _vp]),
     "mrf_profiler_enable": (_i, [_i]),
     "mrf_profiler_read": (_i, [_i, C.POINTER(C.c_double), _i64p]),
 }

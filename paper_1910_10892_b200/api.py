@@ -406,3 +406,16 @@ def iterate_energy(engine: str, mrf: MRF, iterations: int, eval_topo: GridTopolo
         _, labels = eng.aggregate(stream)
         out.append(energy(mrf, labels, eval_topo, stream))
     return out
+
+
+def sgm_forward(mrf: MRF, variant: str = "standard", stream=None):
+    """mp::sgm_forward (baselines.hpp:31-98): returns (cost [B,N,L], labels
+    [B,N] int16, messages [B,R,N,L]). 'revised' is one ISGMR iteration."""
+    t = mrf.topo
+    v = {"standard": 0, "revised": 1}[variant]
+    msgs = torch.empty((mrf.batch, t.num_dirs, t.nodes, mrf.labels), dtype=torch.float32, device=mrf.unary.device)
+    cost = torch.empty_like(mrf.unary)
+    labels = torch.empty((mrf.batch, t.nodes), dtype=torch.int16, device=mrf.unary.device)
+    pr = mrf.c_problem()
+    check(lib().mrf_sgm_f32(t.handle, C.byref(pr), v, _ptr(msgs), _ptr(cost), _ptr(labels), _stream(stream)))
+    return cost, labels, msgs

@@ -13,7 +13,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-UNITS = ["mrf_cuda.cu", "misc.cu", "head.cu", "topology.cpp", "fwd_generic.cu", "fwd_band2_isgmr.cu", "fwd_band2_trwp.cu", "fwd_bandw.cu", "fwd_small.cu",
+UNITS = ["mrf_cuda.cu", "misc.cu", "head.cu", "sgm.cu", "topology.cpp", "fwd_generic.cu", "fwd_band2_isgmr.cu", "fwd_band2_trwp.cu", "fwd_bandw.cu", "fwd_small.cu",
          "bwd_isgmr.cu", "bwd_trwp.cu"]
 OUT = os.path.join(HERE, "libmrf_cuda.so")
 OBJDIR = os.path.join(ROOT, "build", "mrf_cuda")

@@ -29,6 +29,8 @@ cudaError_t launch_energy(int B, int H, int W, int L, int R, const EvenSteps& st
                           float w, const float* wplanes, const uint16_t* labels, double* out, double* partial, int nblk,
                           int* bad, cudaStream_t s);
 int energy_blocks(int N);
+cudaError_t launch_sgm_standard(const Geometry& g, const Potentials& pot, const LineDesc* lines, int nlines, float* m,
+                                int batch, cudaStream_t s);
 
 // backward kernel choice: one warp per line (L <= 32, many lines) or warp-specialised
 inline bool bwd_uses_small(int L, int nlines, int batch) { return L <= 32 && int64_t(nlines) * batch >= 148 * 16; }

@@ -16,7 +16,7 @@
 #include "../../include/mrf_cuda.h"
 #include "common.cuh"
 #include "launch.hpp"
-#include "kernels_v1.cuh"  // aggregate + broadcast helpers
+#include "aggregate.cuh"
 #include "topology.hpp"
 
 using namespace mrf;
@@ -607,6 +607,45 @@ int mrf_energy_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const uint1
     cuda_check(cudaFreeAsync(partial, stream), "cudaFreeAsync");
     cuda_check(cudaStreamSynchronize(stream), "energy sync");
     if (hbad) fail(MRF_EINVAL, "energy: label out of range");
+  });
+}
+
+int mrf_sgm_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int variant, float* messages, float* cost,
+                uint16_t* labels, cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (!messages) fail(MRF_EINVAL, "sgm_forward: null messages");
+    const int R = topo->host.num_dirs(), N = topo->host.nodes();
+    if (variant == 1) {  // revised == one ISGMR iteration
+      const size_t E = size_t(prob->batch) * topo->host.total_edges();
+      uint8_t* pq = nullptr;
+      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&pq), E * (prob->labels + 1), stream), "cudaMallocAsync(p, q)");
+      float* other = nullptr;
+      const size_t mb = messages_bytes(topo, prob);
+      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&other), mb, stream), "cudaMallocAsync(mhat)");
+      cuda_check(cudaMemsetAsync(other, 0, mb, stream), "zero m");
+      cuda_check(cudaMemsetAsync(messages, 0, mb, stream), "zero mhat");
+      PairDescHolder desc(prob, R, stream);
+      isgmr_step(topo, prob, 0, 1, other, messages, pq, pq + E * prob->labels, desc.get(), stream);
+      launch_aggregate(prob, R, N, messages, cost, labels, stream);
+      cuda_check(cudaFreeAsync(other, stream), "cudaFreeAsync");
+      cuda_check(cudaFreeAsync(pq, stream), "cudaFreeAsync");
+    } else if (variant == 0) {
+      const Geometry g = make_geometry(topo, prob, 1);
+      {
+        ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
+        cuda_check(launch_sgm_standard(g, make_potentials(prob), topo->device_lines() + topo->every_start,
+                                       int(topo->every_line.size()), messages, prob->batch, stream),
+                   "sgm_standard launch");
+      }
+      if (cost || labels) {
+        mrf_problem_f32 p2 = *prob;
+        p2.unary = nullptr;  // cost = sum_r m^r (baselines.hpp:84-93)
+        launch_aggregate(&p2, R, N, messages, cost, labels, stream);
+      }
+    } else {
+      fail(MRF_EINVAL, "sgm_forward: unknown variant");
+    }
   });
 }
 

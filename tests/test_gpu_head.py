@@ -114,3 +114,29 @@ def test_iterate_energy_on_4_connected_protocol(engine):
         ref = O.forward(engine, pr, k + 1)
         want = _numpy_energy(H, W, L, 4, un, V, wc, None, ref.labels.astype(np.int64))
         assert abs(es[k][0] - want) <= 1e-9 * max(1.0, abs(want))
+
+
+SGM_CASES = [(6, 7, 5, 4, False, True), (9, 8, 16, 8, True, True), (7, 9, 21, 4, True, False), (5, 6, 40, 4, False, False)]
+
+
+@pytest.mark.parametrize("H,W,L,conn,per_edge,explicit", SGM_CASES)
+def test_sgm_matches_reference(H, W, L, conn, per_edge, explicit):
+    """mp::sgm_forward (baselines.hpp:31-98): standard bit-exact against the
+    reference library; revised == one ISGMR iteration (test_baselines.cpp:58-68)."""
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=H * W + L, per_edge=per_edge, explicit=explicit)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    mrf = to_mrf(pr)
+    cost, labels, msgs = api.sgm_forward(mrf, "revised")
+    ref = O.forward("isgmr", pr, 1)
+    assert np.array_equal(cost[0].cpu().numpy().reshape(-1).view(np.uint32), ref.cost.view(np.uint32))
+    assert np.array_equal(msgs[0].cpu().numpy().reshape(-1).view(np.uint32), ref.messages.view(np.uint32))
+    assert np.array_equal(labels[0].cpu().numpy().view(np.uint16), ref.labels)
+    if not O.have_ref():
+        pytest.skip("reference library not present")
+    c_ref, l_ref, m_ref = O.ref_sgm_standard(pr)
+    cost, labels, msgs = api.sgm_forward(mrf, "standard")
+    assert np.array_equal(msgs[0].cpu().numpy().reshape(-1).view(np.uint32), m_ref.view(np.uint32))
+    assert np.array_equal(cost[0].cpu().numpy().reshape(-1).view(np.uint32), c_ref.view(np.uint32))
+    assert np.array_equal(labels[0].cpu().numpy().view(np.uint16), l_ref)
+    c_rev, _ = O.ref_sgm_revised(pr)
+    assert np.array_equal(c_rev.view(np.uint32), ref.cost.view(np.uint32))
