@@ -457,11 +457,11 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           const int d = mu[i] - (l0 + i);
           near[i] = valid && uint32_t(d + (WIN ? kWin : 1)) <= uint32_t(WIN ? 2 * kWin : 2);
           far[i] = valid && !near[i];
-          if (!WIN) {
-            mword |= (valid && d == -1 ? 1u : 0u) << i;
-            mword |= (valid && d == 0 ? 1u : 0u) << (8 + i);
-            mword |= (valid && d == 1 ? 1u : 0u) << (16 + i);
-          }
+          // targets l-1 / l / l+1 go through registers in every mode (the
+          // window masks carry only 2 <= |d| <= kWin)
+          mword |= (valid && d == -1 ? 1u : 0u) << i;
+          mword |= (valid && d == 0 ? 1u : 0u) << (8 + i);
+          mword |= (valid && d == 1 ? 1u : 0u) << (16 + i);
           kmn = far[i] ? min(kmn, mu[i]) : kmn;
           kmx = far[i] ? max(kmx, mu[i]) : kmx;
         }
@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           __syncwarp();
 #pragma unroll
           for (int i = 0; i < EPL; ++i)
-            if (near[i]) atomicOr(wmk + mu[i], 1u << (kWin - (mu[i] - (l0 + i))));
+            if (near[i] && uint32_t(mu[i] - (l0 + i) + 1) > 2u) atomicOr(wmk + mu[i], 1u << (kWin - (mu[i] - (l0 + i))));
           __syncwarp();
           uint32_t wm[EPL];
 #pragma unroll
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           window_gather<EPL>(B, wm, l0, [&](int l) { return xr[l]; });
         }
         if (!early) {
-          scatter_row<EPL, !WIN>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
+          scatter_row<EPL>(B, x, mword, main_t, noth, olist, sl + SL::CIN, lane);  // CIN: reduction scratch
           qfix();
         }
         __syncwarp();
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           __syncwarp();
           window_gather<EPL>(acc, wm, l0, [&](int l) { return s_c[pidx<EPL>(l)]; });
         }
-        scatter_row<EPL, !WIN>(acc, carry, mword, main_t, noth, reinterpret_cast<const uint16_t*>(sl + SL::OTH), s_red,
+        scatter_row<EPL>(acc, carry, mword, main_t, noth, reinterpret_cast<const uint16_t*>(sl + SL::OTH), s_red,
                                lane);
         sts_slice<EPL>(sl + SL::CIN + l0, carry);
         sts_slice<EPL>(sl + SL::ACC + l0, acc);
