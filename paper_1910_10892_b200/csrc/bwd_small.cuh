@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     const bool fuse = TRWP && a.dtheta != nullptr;
     float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
     const uint32_t ebase = uint32_t(a.k) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
+    const float* rowb[NRMAX];  // this lane's element of each staged row, at node 0
+#pragma unroll
+    for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] = sd[rr] < 0 ? dcb : ainb + size_t(sd[rr] > 0 ? sd[rr] : 0) * NL;
 
     auto issue = [&](int s) {
       const uint32_t base_s = ring_s + 4u * uint32_t((s % kStages) * stage_f);
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr)
           if (rr < nrows)
-            cp_async_u32(base_s + 4u * (rr * 32 + lane), (sd[rr] < 0 ? dcb : ainb + size_t(sd[rr]) * NL) + ocur, 4);
+            cp_async_u32(base_s + 4u * (rr * 32 + lane), rowb[rr] + ocur, 4);
       }
       const uint32_t e = ebase + uint32_t(j - 1);
       const size_t pb = size_t(e) * L;

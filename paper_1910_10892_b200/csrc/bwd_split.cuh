@@ -308,9 +308,9 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
       const int a0 = first ? 1 : 0;  // first plane slot
       const int npl = nrows;         // plane rows end here
       const bool fuse = TRWP && a.dtheta != nullptr;
-      int soff[NRMAX];
+      const float* rowb[NRMAX];  // each staged row at node 0
 #pragma unroll
-      for (int rr = 0; rr < NRMAX; ++rr) soff[rr] = sd[rr] < 0 ? 0 : sd[rr] * NL;
+      for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] = sd[rr] < 0 ? dcb : ainb + size_t(sd[rr] > 0 ? sd[rr] : 0) * NL;
 
       // this warp's steps: s = pw, pw + NPRE, ...; local index t = s / NPRE
       const int nmine = nsteps > pw ? (nsteps - pw + NPRE - 1) / NPRE : 0;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr) {
           if (rr < nrows) {
-            const float* src = (sd[rr] < 0 ? dcb : ainb + soff[rr]) + ocur;
+            const float* src = rowb[rr] + ocur;
             if (FULL) {  // the row is 8*EPL 16-byte chunks
 #pragma unroll
               for (int u = lane; u < 8 * EPL; u += 32) cp_async_u32(base_s + 4u * (rr * LS) + 16u * u, src + 4 * u, 16);
