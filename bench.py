@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -279,7 +279,6 @@ def main():
     barrier()
     torch.cuda.synchronize()
 
-    _lib.check(_lib.lib().mrf_profiler_enable(1))
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
@@ -291,6 +290,13 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
+    # per-kernel-class device time (roofline): a second pass of the same K
+    # steps with the library's launch profiler on (events around every
+    # launch), kept out of the timed region above
+    _lib.check(_lib.lib().mrf_profiler_enable(1))
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     prof = {}
     import ctypes as C
     for cls in range(4):

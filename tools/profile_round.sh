@@ -20,3 +20,9 @@ $NCU -k regex:bwd_split_kernel -s 0 -c 1 -o gpurun_out/ncu_bwdV_C2_${TAG} python
 $NCU -k regex:bwd_split_kernel -s 6 -c 1 -o gpurun_out/ncu_bwdH_C2_${TAG} python tools/prof_run.py C2 1 > /dev/null 2>&1
 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_C2_${TAG}.json 2> gpurun_out/bench_C2_${TAG}.err
 tail -1 gpurun_out/bench_C2_${TAG}.json
+# summaries for profiles/ (the .ncu-rep files stay on the box: gpurun brings back <= 64 MiB)
+for k in fwdH fwdV bwdH bwdV; do
+  python tools/ncu_summary.py full gpurun_out/ncu_${k}_C2_${TAG}.ncu-rep gpurun_out/ncu_${k}_C2_${TAG}.json "C2 $k ${TAG}"
+done
+python tools/ncu_summary.py launches gpurun_out/launches_C2_${TAG}.csv gpurun_out/launches_C2_${TAG}.json
+rm -f gpurun_out/*.ncu-rep
