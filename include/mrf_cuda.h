@@ -211,6 +211,10 @@ int mrf_sgm_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int variant, f
  * returns the summed device time and launch count of one kernel class. */
 int mrf_profiler_enable(int on);
 int mrf_profiler_read(int kernel_class, double* total_ms, int64_t* launches);
+/* Number of kernel launches this library has made since it was loaded
+ * (including the launches a sweep makes for strategies that do not own it and
+ * exit at once). */
+int mrf_launch_count(int64_t* total);
 
 #ifdef __cplusplus
 }

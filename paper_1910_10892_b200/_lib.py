@@ -69,6 +69,7 @@ SIGNATURES = {
     "mrf_sgm_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _vp]),
     "mrf_profiler_enable": (_i, [_i]),
     "mrf_profiler_read": (_i, [_i, C.POINTER(C.c_double), _i64p]),
+    "mrf_launch_count": (_i, [_i64p]),
 }
 KCLASS_FWD_SWEEP, KCLASS_BWD_SWEEP, KCLASS_AGGREGATE, KCLASS_AUX = 0, 1, 2, 3
 

@@ -17,7 +17,7 @@ static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = a.nlines < 65535 ? a.nlines : 65535;
-  kern<<<dim3(blocks, batch), 32 * (2 + NPRE), smem, s>>>(a);
+  kern<<<dim3(blocks, batch), 32 * (2 + NPRE), smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }
 
@@ -48,7 +48,7 @@ static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
-  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }
 

@@ -15,7 +15,7 @@ static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
-  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a);
+  kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }
 

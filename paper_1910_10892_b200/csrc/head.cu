@@ -140,8 +140,8 @@ __global__ void finish_sum_kernel(int B, int nblk, const double* __restrict__ pa
 
 cudaError_t launch_soft_head(int B, int N, int L, const float* cost, const float* target, float* conf, float* disp,
                              float* grad, float* loss, double* partial, int nblk, cudaStream_t s) {
-  soft_head_kernel<<<dim3(nblk, B), 32 * kHeadWarps, 0, s>>>(N, L, cost, target, conf, disp, grad, partial);
-  finish_mean_kernel<<<(B + 127) / 128, 128, 0, s>>>(B, nblk, N, partial, loss);
+  soft_head_kernel<<<dim3(nblk, B), 32 * kHeadWarps, 0, s>>>(N, L, cost, target, conf, disp, grad, partial); note_launch();
+  finish_mean_kernel<<<(B + 127) / 128, 128, 0, s>>>(B, nblk, N, partial, loss); note_launch();
   return cudaGetLastError();
 }
 
@@ -150,8 +150,8 @@ int soft_head_blocks(int N) { return std::max(1, std::min(148 * 8, (N + kHeadWar
 cudaError_t launch_energy(int B, int H, int W, int L, int R, const EvenSteps& st, const float* unary, const float* V,
                           float w, const float* wplanes, const uint16_t* labels, double* out, double* partial, int nblk,
                           int* bad, cudaStream_t s) {
-  energy_kernel<<<dim3(nblk, B), 256, 0, s>>>(H, W, L, R, st, unary, V, w, wplanes, labels, partial, bad);
-  finish_sum_kernel<<<(B + 127) / 128, 128, 0, s>>>(B, nblk, partial, out);
+  energy_kernel<<<dim3(nblk, B), 256, 0, s>>>(H, W, L, R, st, unary, V, w, wplanes, labels, partial, bad); note_launch();
+  finish_sum_kernel<<<(B + 127) / 128, 128, 0, s>>>(B, nblk, partial, out); note_launch();
   return cudaGetLastError();
 }
 

@@ -9,6 +9,9 @@
 
 namespace mrf {
 
+// every kernel launch of the library is counted (mrf_launch_count)
+void note_launch();
+
 // labels per lane for the warp-per-scanline kernels
 inline int epl_for(int L) {
   if (L <= 32) return 1;

@@ -2,6 +2,8 @@
 // data-parallel collective (NCCL all-reduce, resolved at run time).
 #include <dlfcn.h>
 
+#include <atomic>
+
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -11,6 +13,10 @@
 #include "launch.hpp"
 
 namespace mrf {
+
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+int64_t launch_total() { return g_launches.load(std::memory_order_relaxed); }
 
 cudaError_t ensure_dynamic_smem(const void* kern, int bytes) {
   static std::mutex mu;
@@ -77,7 +83,10 @@ int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaS
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? MRF_ENOMEM : MRF_ECUDA;
   const int one = 1;
   cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, stream);
-  if (count) finite_kernel<<<1184, 256, 0, stream>>>(data, count, dflag);
+  if (count) {
+    finite_kernel<<<1184, 256, 0, stream>>>(data, count, dflag);
+    mrf::note_launch();
+  }
   int h = 0;
   cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream);
   cudaFreeAsync(dflag, stream);
@@ -93,6 +102,7 @@ int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const m
   const int64_t plane_elems = int64_t(num_dirs / 2) * prob->height * prob->width;
   pack_kernel<<<1, 1024, 0, stream>>>(prob->batch, prob->labels, plane_elems, grads->pairwise, grads->weight_planes,
                                       out);
+  mrf::note_launch();
   return cudaGetLastError() == cudaSuccess ? MRF_OK : MRF_ECUDA;
 }
 
@@ -112,3 +122,9 @@ int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaSt
 }
 
 }  // extern "C"
+
+extern "C" int mrf_launch_count(int64_t* total) {
+  if (!total) return MRF_EINVAL;
+  *total = mrf::launch_total();
+  return MRF_OK;
+}

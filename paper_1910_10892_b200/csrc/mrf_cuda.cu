@@ -242,12 +242,12 @@ class PairDescHolder {
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_), sizeof(PairDesc), s), "cudaMallocAsync(desc)");
     const int64_t planes = int64_t(pr->batch) * (R / 2) * pr->height * pr->width;
     ProfScope ps(s, MRF_KCLASS_AUX);
-    analyze_pairwise_kernel<<<1, 1024, 0, s>>>(pr->pairwise, pr->labels, pr->weight, pr->weight_planes != nullptr, d_);
+    analyze_pairwise_kernel<<<1, 1024, 0, s>>>(pr->pairwise, pr->labels, pr->weight, pr->weight_planes != nullptr, d_); note_launch();
     cuda_check(cudaGetLastError(), "analyze_pairwise launch");
     for (const float* pl : {pr->weight_planes, pr->rho_planes}) {
       if (!pl) continue;
       const int blocks = int(std::min<int64_t>(148 * 4, (planes + 255) / 256));
-      scan_neg_zero_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(pl), planes, d_);
+      scan_neg_zero_kernel<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint32_t*>(pl), planes, d_); note_launch();
       cuda_check(cudaGetLastError(), "scan_neg_zero launch");
     }
   }
@@ -289,7 +289,7 @@ void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* mess
   const int64_t blocks = (warps + per_block - 1) / per_block;
   ProfScope ps(stream, MRF_KCLASS_AGGREGATE);
   aggregate_kernel<<<unsigned(blocks), per_block * 32, 0, stream>>>(pr->batch, N, pr->labels, R, pr->unary, messages,
-                                                                    cost, labels);
+                                                                    cost, labels); note_launch();
   cuda_check(cudaGetLastError(), "aggregate_kernel launch");
 }
 
@@ -368,7 +368,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       }
       if (!fuse) {
         ProfScope ps(stream, MRF_KCLASS_AUX);
-        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary);
+        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary); note_launch();
         cuda_check(cudaGetLastError(), "dtheta_acc launch");
       }
     } else {
@@ -380,20 +380,20 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       }
       // ISGMR's directions run concurrently: the unary gradient is collected after the launch
       ProfScope ps(stream, MRF_KCLASS_AUX);
-      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary);
+      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary); note_launch();
       cuda_check(cudaGetLastError(), "dtheta_acc launch");
     }
   }
   if (isgmr_dw) {
     ProfScope ps(stream, MRF_KCLASS_AUX);
     combine_dw_kernel<<<int(std::min<int64_t>(148 * 4, (int64_t(B) * (R / 2) * N + 255) / 256)), 256, 0, stream>>>(
-        B, R, N, dwr, grads->weight_planes);
+        B, R, N, dwr, grads->weight_planes); note_launch();
     cuda_check(cudaGetLastError(), "combine_dw launch");
   }
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
     ProfScope ps(stream, MRF_KCLASS_AUX);
-    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, gvacc, grads->pairwise);
+    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, gvacc, grads->pairwise); note_launch();
     cuda_check(cudaGetLastError(), "reduce_gvacc launch");
   }
 }

@@ -94,7 +94,7 @@ cudaError_t run(const Geometry& g, const Potentials& pot, const LineDesc* lines,
                 cudaStream_t s) {
   const int wpc = 4;
   const int blocks = (nlines + wpc - 1) / wpc < 65535 ? (nlines + wpc - 1) / wpc : 65535;
-  sgm_standard_kernel<EPL><<<dim3(blocks, batch), 32 * wpc, sizeof(float) * 32 * EPL * wpc, s>>>(g, pot, lines, nlines, m);
+  sgm_standard_kernel<EPL><<<dim3(blocks, batch), 32 * wpc, sizeof(float) * 32 * EPL * wpc, s>>>(g, pot, lines, nlines, m); note_launch();
   return cudaGetLastError();
 }
 
