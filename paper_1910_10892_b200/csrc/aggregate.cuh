@@ -5,13 +5,18 @@
 #pragma once
 
 #include "common.cuh"
+#include "fwd_warp.cuh"
 
 namespace mrf {
 
 // c = theta + sum_r m^r (r ascending) and labels = first argmin
 // (inference.hpp:25-57). One warp per node.
+// fused_by_band2: the banded D == 2 forward kernel already wrote cost /
+// labels during the last sweep when it owned the call (PairDesc).
 __global__ void aggregate_kernel(int B, int N, int L, int R, const float* __restrict__ unary,
-                                 const float* __restrict__ m, float* __restrict__ cost, uint16_t* __restrict__ labels) {
+                                 const float* __restrict__ m, float* __restrict__ cost, uint16_t* __restrict__ labels,
+                                 const PairDesc* __restrict__ desc, int fused_by_band2) {
+  if (fused_by_band2 && desc->banded && desc->D == 2) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gw >= int64_t(B) * N) return;

@@ -38,7 +38,27 @@ __device__ __forceinline__ void store_p(uint8_t* row, int l0, const int (&am)[EP
   }
 }
 
-template <int EPL, bool TRWP, int R, bool FULL>
+// aggregate_costs + argmin_labels (inference.hpp:25-57) of one node from its
+// already summed cost row c = theta + sum_r m^r (r ascending).
+template <int EPL, bool FULL>
+__device__ __forceinline__ void agg_node(const FwdArgs& a, size_t node_row, size_t label_idx, const float (&c)[EPL],
+                                         int l0, int nvalid, int L, int lane) {
+  if (a.agg_cost) stg_slice<EPL>(a.agg_cost + node_row, l0, c, FULL ? EPL : nvalid, L);
+  uint32_t bk = 0xffffffffu, bt = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < EPL; ++i) {
+    const uint32_t kk = (FULL || i < nvalid) ? order_key(fadd(c[i], 0.0f)) : 0xffffffffu;
+    const bool t = kk < bk;
+    bk = t ? kk : bk;
+    bt = t ? uint32_t(l0 + i) : bt;
+  }
+  const uint32_t kmin = __reduce_min_sync(0xffffffffu, bk);
+  const uint32_t tmin = __reduce_min_sync(0xffffffffu, bk == kmin ? bt : 0xffffffffu);
+  if (lane == 0 && a.agg_labels) a.agg_labels[label_idx] = uint16_t(tmin);
+}
+
+// AGG (TRWP, last sweep only): also aggregate cost / labels on the fly
+template <int EPL, bool TRWP, int R, bool FULL, bool AGG = false>
 __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   if (!(a.desc->banded && a.desc->D == 2)) return;  // fwd_warp_kernel handles it
   extern __shared__ float smem[];
@@ -143,6 +163,12 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
           }
 #pragma unroll
           for (int i = 0; i < EPL; ++i) base[i] = fsub(fmul(rho, s[i]), mo[i]);
+          // last sweep (r == R-1, carry = the new m^r): s is node prev's
+          // aggregated cost in the reference's order
+          if (AGG) {
+            const int prev = ld.first + (j - 1) * st;
+            agg_node<EPL, FULL>(a, (size_t(b) * N + prev) * L, size_t(b) * N + prev, s, l0, nvalid, L, lane);
+          }
         }
       }
       if (!FULL) {
@@ -379,6 +405,22 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       const int cur = ld.first + j * st;
       stg_slice<EPL>(mout + size_t(cur) * L, l0, carry, FULL ? EPL : nvalid, L);
       if (lane == 0) a.q[pq_base + j - 1] = uint8_t(qmin);
+    }
+    if (TRWP && AGG) {
+      // the tail is no edge's prev: its cost from its rows and the final message
+      const int tail = ld.first + nsteps * st;
+      float c[EPL], t[EPL];
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) c[i] = (FULL || i < nvalid) ? __ldcg(un + size_t(tail) * L + l0 + i) : 0.0f;
+#pragma unroll
+      for (int d = 0; d < R; ++d) {
+#pragma unroll
+        for (int i = 0; i < EPL; ++i)
+          t[i] = d == r ? carry[i] : ((FULL || i < nvalid) ? __ldcg(a.m_in + img + (size_t(d) * N + tail) * L + l0 + i) : 0.0f);
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) c[i] = fadd(c[i], t[i]);
+      }
+      agg_node<EPL, FULL>(a, (size_t(b) * N + tail) * L, size_t(b) * N + tail, c, l0, nvalid, L, lane);
     }
     cp_wait<0>();
     __syncwarp();

@@ -93,6 +93,10 @@ struct FwdArgs {
   int band2_launched;  // fwd_band2_kernel covers banded D == 2 in this sweep
   int bandw_max;       // fwd_bandw_kernel covers banded 2 < D <= bandw_max (0: not launched)
   int dense_small;     // fwd_small_kernel covers dense V with L <= 32
+  // TRWP, last sweep of the last iteration (4 directions): the banded D == 2
+  // kernel also writes the aggregated cost / labels (else null)
+  float* agg_cost;
+  uint16_t* agg_labels;
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {

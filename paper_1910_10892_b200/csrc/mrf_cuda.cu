@@ -262,7 +262,7 @@ class PairDescHolder {
 template <bool TRWP>
 void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines, int nlines,
                           const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k, const PairDesc* desc,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, float* agg_cost = nullptr, uint16_t* agg_labels = nullptr) {
   if (nlines == 0) return;
   // The pairwise strategy is only known on the device (desc), so the banded
   // D == 2 specialisation and the generic kernel are both launched; each
@@ -270,7 +270,7 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
   const bool band2 = g.R == 4 || g.R == 8;
   const bool small = fwd_small_applies(g.L, g.R);
   FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0, band2 ? fwd_bandw_max() : 0,
-            small ? 1 : 0};
+            small ? 1 : 0, agg_cost, agg_labels};
   ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
   if (band2) {
     cuda_check(TRWP ? launch_fwd_band2_trwp(a, pr->batch, stream) : launch_fwd_band2_isgmr(a, pr->batch, stream),
@@ -282,14 +282,15 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
 }
 
 void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* messages, float* cost, uint16_t* labels,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, const PairDesc* desc = nullptr, bool fused_by_band2 = false) {
   if (!cost && !labels) return;
   const int64_t warps = int64_t(pr->batch) * N;
   const int per_block = 8;
   const int64_t blocks = (warps + per_block - 1) / per_block;
   ProfScope ps(stream, MRF_KCLASS_AGGREGATE);
   aggregate_kernel<<<unsigned(blocks), per_block * 32, 0, stream>>>(pr->batch, N, pr->labels, R, pr->unary, messages,
-                                                                    cost, labels); note_launch();
+                                                                    cost, labels, desc, fused_by_band2 ? 1 : 0);
+  note_launch();
   cuda_check(cudaGetLastError(), "aggregate_kernel launch");
 }
 
@@ -301,12 +302,12 @@ void isgmr_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap
 }
 
 void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap, float* m, uint8_t* p, uint8_t* q,
-               const PairDesc* desc, cudaStream_t stream) {
+               const PairDesc* desc, cudaStream_t stream, float* agg_cost = nullptr, uint16_t* agg_labels = nullptr) {
   const Geometry g = make_geometry(topo, pr, K_cap);
   const LineDesc* lines = topo->device_lines();
   for (int r = 0; r < g.R; ++r)  // directions strictly sequential (trwp.hpp:50)
     launch_forward_sweep<true>(pr, g, lines + topo->dir_start[r], int(topo->dir_lines[r].size()), m, m, p, q, k, desc,
-                               stream);
+                               stream, r == g.R - 1 ? agg_cost : nullptr, r == g.R - 1 ? agg_labels : nullptr);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -491,9 +492,16 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
     cuda_check(cudaMemsetAsync(out->messages, 0, messages_bytes(topo, prob), stream), "zero m");
     PairDescHolder desc(prob, topo->host.num_dirs(), stream);
-    for (int k = 0; k < iterations; ++k)
-      trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, desc.get(), stream);
-    launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
+    // 4 directions: the last sweep's banded D == 2 kernel aggregates on the
+    // fly (every node is a prev or the tail of one of its lines)
+    const bool fuse = topo->host.num_dirs() == 4 && (out->cost || out->labels);
+    for (int k = 0; k < iterations; ++k) {
+      const bool last = fuse && k == iterations - 1;
+      trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, desc.get(), stream,
+                last ? out->cost : nullptr, last ? out->labels : nullptr);
+    }
+    launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream,
+                     desc.get(), fuse);
   });
 }
 
