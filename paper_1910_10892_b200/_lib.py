@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmrf_cuda.so")
+LIB_PATH = os.environ.get("MRF_LIB_PATH") or os.path.join(HERE, "libmrf_cuda.so")  # override: A/B builds
 
 MRF_OK, MRF_EINVAL, MRF_ECUDA, MRF_ENOMEM = 0, 1, 2, 3
 ENGINE_ISGMR, ENGINE_TRWP = 0, 1

@@ -57,8 +57,10 @@ __device__ __forceinline__ void agg_node(const FwdArgs& a, size_t node_row, size
   if (lane == 0 && a.agg_labels) a.agg_labels[label_idx] = uint16_t(tmin);
 }
 
-// AGG (TRWP, last sweep only): also aggregate cost / labels on the fly
-template <int EPL, bool TRWP, int R, bool FULL, bool AGG = false>
+// AGG (TRWP, last sweep only): also aggregate cost / labels on the fly.
+// RD >= 0: every line of the launch sweeps direction RD (TRWP launches one
+// direction at a time), so the row selection below folds at compile time.
+template <int EPL, bool TRWP, int R, bool FULL, bool AGG = false, int RD = -1>
 __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   if (!(a.desc->banded && a.desc->D == 2)) return;  // fwd_warp_kernel handles it
   extern __shared__ float smem[];
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
 
   for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
     const LineDesc ld = a.lines[li];
-    const int r = ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
+    const int r = RD >= 0 ? RD : ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
     const int nsteps = ld.length - 1;
     const float* rowp[ROWS];
     rowp[0] = un + l0;

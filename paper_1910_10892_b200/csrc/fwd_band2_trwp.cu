@@ -4,12 +4,12 @@
 
 namespace mrf {
 
-template <int EPL, int R, bool FULL, bool AGG = false>
+template <int EPL, int R, bool FULL, bool AGG = false, int RD = -1>
 static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
   constexpr int rows = 1 + (true ? R - 1 : R - 2);
   const int wpc = warps_per_cta(a.nlines);
   const int smem = band2_smem_floats(EPL, rows) * int(sizeof(float)) * wpc;
-  auto kern = fwd_band2_kernel<EPL, true, R, FULL, AGG>;
+  auto kern = fwd_band2_kernel<EPL, true, R, FULL, AGG, RD>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
@@ -21,9 +21,16 @@ template <int EPL>
 static cudaError_t run_epl(const FwdArgs& a, int batch, cudaStream_t s) {
   const bool full = a.g.L == 32 * EPL;
   if (a.g.R == 4) {
-    if (a.agg_cost || a.agg_labels)  // last sweep of the call: aggregation fused
-      return full ? run<EPL, 4, true, true>(a, batch, s) : run<EPL, 4, false, true>(a, batch, s);
-    return full ? run<EPL, 4, true>(a, batch, s) : run<EPL, 4, false>(a, batch, s);
+    switch (a.dir) {  // one direction per launch: compile-time row selection
+      case 0: return full ? run<EPL, 4, true, false, 0>(a, batch, s) : run<EPL, 4, false, false, 0>(a, batch, s);
+      case 1: return full ? run<EPL, 4, true, false, 1>(a, batch, s) : run<EPL, 4, false, false, 1>(a, batch, s);
+      case 2: return full ? run<EPL, 4, true, false, 2>(a, batch, s) : run<EPL, 4, false, false, 2>(a, batch, s);
+      case 3:
+        if (a.agg_cost || a.agg_labels)  // last sweep of the call: aggregation fused
+          return full ? run<EPL, 4, true, true, 3>(a, batch, s) : run<EPL, 4, false, true, 3>(a, batch, s);
+        return full ? run<EPL, 4, true, false, 3>(a, batch, s) : run<EPL, 4, false, false, 3>(a, batch, s);
+      default: return full ? run<EPL, 4, true>(a, batch, s) : run<EPL, 4, false>(a, batch, s);
+    }
   }
   return full ? run<EPL, 8, true>(a, batch, s) : run<EPL, 8, false>(a, batch, s);
 }

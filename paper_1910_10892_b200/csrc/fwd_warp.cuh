@@ -97,6 +97,7 @@ struct FwdArgs {
   // kernel also writes the aggregated cost / labels (else null)
   float* agg_cost;
   uint16_t* agg_labels;
+  int dir;  // the one direction every line of the launch sweeps (TRWP), -1: mixed (ISGMR)
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {

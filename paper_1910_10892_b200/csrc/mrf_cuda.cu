@@ -262,7 +262,8 @@ class PairDescHolder {
 template <bool TRWP>
 void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const LineDesc* lines, int nlines,
                           const float* m_in, float* m_out, uint8_t* p, uint8_t* q, int k, const PairDesc* desc,
-                          cudaStream_t stream, float* agg_cost = nullptr, uint16_t* agg_labels = nullptr) {
+                          cudaStream_t stream, float* agg_cost = nullptr, uint16_t* agg_labels = nullptr,
+                          int dir = -1) {
   if (nlines == 0) return;
   // The pairwise strategy is only known on the device (desc), so the banded
   // D == 2 specialisation and the generic kernel are both launched; each
@@ -270,7 +271,7 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
   const bool band2 = g.R == 4 || g.R == 8;
   const bool small = fwd_small_applies(g.L, g.R);
   FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0, band2 ? fwd_bandw_max() : 0,
-            small ? 1 : 0, agg_cost, agg_labels};
+            small ? 1 : 0, agg_cost, agg_labels, dir};
   ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
   if (band2) {
     cuda_check(TRWP ? launch_fwd_band2_trwp(a, pr->batch, stream) : launch_fwd_band2_isgmr(a, pr->batch, stream),
@@ -307,7 +308,7 @@ void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap,
   const LineDesc* lines = topo->device_lines();
   for (int r = 0; r < g.R; ++r)  // directions strictly sequential (trwp.hpp:50)
     launch_forward_sweep<true>(pr, g, lines + topo->dir_start[r], int(topo->dir_lines[r].size()), m, m, p, q, k, desc,
-                               stream, r == g.R - 1 ? agg_cost : nullptr, r == g.R - 1 ? agg_labels : nullptr);
+                               stream, r == g.R - 1 ? agg_cost : nullptr, r == g.R - 1 ? agg_labels : nullptr, r);
 }
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
