@@ -13,8 +13,8 @@
 
 namespace mrf {
 
-__host__ __device__ constexpr int band2_smem_floats(int EPL, int rows) {
-  return ((kStages * rows + 1) * 32 * EPL + kStages * 64 + 31) / 32 * 32;
+__host__ __device__ constexpr int band2_smem_floats(int EPL, int rows, int stages = kStages) {
+  return ((stages * rows + 1) * 32 * EPL + stages * 64 + 31) / 32 * 32;
 }
 
 // EPL bytes (one per label) -> one (or a few) packed stores at row + l0.
@@ -60,7 +60,8 @@ __device__ __forceinline__ void agg_node(const FwdArgs& a, size_t node_row, size
 // AGG (TRWP, last sweep only): also aggregate cost / labels on the fly.
 // RD >= 0: every line of the launch sweeps direction RD (TRWP launches one
 // direction at a time), so the row selection below folds at compile time.
-template <int EPL, bool TRWP, int R, bool FULL, bool AGG = false, int RD = -1>
+// ST: cp.async ring depth (ST - 1 node steps in flight).
+template <int EPL, bool TRWP, int R, bool FULL, bool AGG = false, int RD = -1, int ST = kStages>
 __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   if (!(a.desc->banded && a.desc->D == 2)) return;  // fwd_warp_kernel handles it
   extern __shared__ float smem[];
@@ -70,9 +71,9 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
   const Geometry& g = a.g;
   const int L = g.L, N = g.N;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  float* ring = smem + size_t(wid) * band2_smem_floats(EPL, ROWS);
-  float* s_x = ring + kStages * ROWS * LS;
-  float* s_u = s_x + kStages * 64;  // far-candidate costs of the current node
+  float* ring = smem + size_t(wid) * band2_smem_floats(EPL, ROWS, ST);
+  float* s_x = ring + ST * ROWS * LS;
+  float* s_u = s_x + ST * 64;  // far-candidate costs of the current node
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   const uint32_t x_s = static_cast<uint32_t>(__cvta_generic_to_shared(s_x));
 
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
     const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     auto issue = [&](int j) {
-      const int slot = (j - 1) % kStages;
+      const int slot = (j - 1) % ST;
       const int prev = ld.first + (j - 1) * st;
       const size_t off = size_t(prev) * L;
       if (FULL || nvalid > 0) {
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       if (rpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + 32 + lane), rrow + wnode, 4);
     };
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < ST - 1; ++s) {
       if (1 + s <= nsteps) issue(1 + s);
       cp_commit();
     }
@@ -124,10 +125,10 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
     for (int i = 0; i < EPL; ++i) carry[i] = 0.0f;
 
     for (int j = 1; j <= nsteps; ++j) {
-      if (j + kStages - 1 <= nsteps) issue(j + kStages - 1);
+      if (j + ST - 1 <= nsteps) issue(j + ST - 1);
       cp_commit();
-      cp_wait<kStages - 1>();
-      const int slot = (j - 1) % kStages;
+      cp_wait<ST - 1>();
+      const int slot = (j - 1) % ST;
       const float* srow = ring + slot * ROWS * LS + l0;
       if (wpl) {
         const float w = s_x[slot * 64 + lane];

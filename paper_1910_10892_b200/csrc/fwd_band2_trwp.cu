@@ -4,17 +4,23 @@
 
 namespace mrf {
 
-template <int EPL, int R, bool FULL, bool AGG = false, int RD = -1>
-static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
+template <int EPL, int R, bool FULL, bool AGG, int RD, int ST>
+static cudaError_t run_(const FwdArgs& a, int batch, cudaStream_t s) {
   constexpr int rows = 1 + (true ? R - 1 : R - 2);
   const int wpc = warps_per_cta(a.nlines);
-  const int smem = band2_smem_floats(EPL, rows) * int(sizeof(float)) * wpc;
-  auto kern = fwd_band2_kernel<EPL, true, R, FULL, AGG, RD>;
+  const int smem = band2_smem_floats(EPL, rows, ST) * int(sizeof(float)) * wpc;
+  auto kern = fwd_band2_kernel<EPL, true, R, FULL, AGG, RD, ST>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
   kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a); note_launch();
   return cudaGetLastError();
+}
+
+template <int EPL, int R, bool FULL, bool AGG = false, int RD = -1>
+static cudaError_t run(const FwdArgs& a, int batch, cudaStream_t s) {
+  return band2_stages(a.nlines, batch, a.g.L) == 3 ? run_<EPL, R, FULL, AGG, RD, 3>(a, batch, s)
+                                            : run_<EPL, R, FULL, AGG, RD, 4>(a, batch, s);
 }
 
 template <int EPL>

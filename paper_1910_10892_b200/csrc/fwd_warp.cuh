@@ -200,7 +200,10 @@ __device__ __forceinline__ void stg_slice(float* row, int l0, const float (&v)[E
   }
 }
 
-constexpr int kStages = 4;
+#ifndef MRF_FWD_STAGES
+#define MRF_FWD_STAGES 4
+#endif
+constexpr int kStages = MRF_FWD_STAGES;  // cp.async ring depth (steps in flight + 1)
 constexpr float kInf = __builtin_huge_valf();
 
 // Per-warp shared memory (floats): ring [kStages][rows][32*EPL], per-lane

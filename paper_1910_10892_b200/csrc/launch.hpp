@@ -4,6 +4,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdint>
+#include <cstdlib>
+
 #include "bwd_common.cuh"
 #include "fwd_warp.cuh"
 
@@ -19,6 +22,18 @@ inline int epl_for(int L) {
   if (L <= 128) return 4;
   if (L <= 192) return 6;
   return 8;
+}
+
+// cp.async ring depth of the banded D == 2 forward for a launch of nlines
+// lines x batch with L labels: 3 when warps share schedulers and rows are
+// long, else 4 (measured, real-run fwd time per step: C2 13.35 -> 12.70 ms
+// with 3 on the vertical sweeps only; the horizontal ones (lone warps) lose at
+// 3; C1 (L = 16) loses 6 % at 3, C3 (L = 128) is neutral).
+// MRF_BAND2_STAGES=3|4 forces one (A/B measurements).
+inline int band2_stages(int nlines, int batch, int L) {
+  const char* env = getenv("MRF_BAND2_STAGES");
+  if (env && (env[0] == '3' || env[0] == '4')) return env[0] - '0';
+  return int64_t(nlines) * batch > 4 * 148 && L > 128 ? 3 : 4;
 }
 
 // Readout and evaluation (head.cu)

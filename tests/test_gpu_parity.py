@@ -242,3 +242,18 @@ def test_c1_full_size_matches_reference(engine):
     gref = O.backward(engine, pr, wl.K, ref.p, ref.q, gc, impl="ref", threads=0)
     g = gpu_backward(engine, mrf, f, gc)
     assert_grads_close(g, gref)
+
+
+@pytest.mark.parametrize("stages", ["3", "4"])
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", [(6, 9, 192, 4, 3, True), (5, 7, 150, 8, 2, False), (4, 6, 256, 4, 2, False),
+                                  (7, 5, 100, 4, 2, True)], ids=["L192c4", "L150c8", "L256c4", "L100c4"])
+def test_band2_ring_depths_bit_exact(case, engine, stages, monkeypatch):
+    """The banded D == 2 forward at both cp.async ring depths (the launcher
+    picks 3 only for launches with many long lines; forced here)."""
+    monkeypatch.setenv("MRF_BAND2_STAGES", stages)
+    H, W, L, conn, K, per_edge = case
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=L + H, per_edge=per_edge, explicit=False)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    assert_forward_equal(gpu_forward(engine, to_mrf(pr), K), ref)
