@@ -359,18 +359,22 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       }
 
       // ---- combine in index order: [0,l-2] | l-1 | l | l+1 | [l+2,L)
+      // (an infinite left summary -- l < 2 -- always loses to the finite
+      // near candidates, so its index needs no masking)
       float out[EPL];
       int am[EPL];
+      float nb[EPL];  // base + w g(1): the near candidate of both neighbouring labels
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) nb[i] = fadd(base[i], wg1);
+      const float nbl = fadd(bl, wg1), nbr = fadd(br, wg1);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) {
         const int l = l0 + i;
         const float lv = LV[i], rv = RV[i];
         const int lix = LI[i], rix = RI[i];
-        const float bm1 = i >= 1 ? base[i >= 1 ? i - 1 : 0] : bl;
-        const float bp1 = i + 1 < EPL ? base[i + 1 < EPL ? i + 1 : 0] : br;
         float best = lv;
-        int arg = lv < kInf ? lix : 0;
-        float v = fadd(bm1, wg1);
+        int arg = lix;
+        float v = i >= 1 ? nb[i >= 1 ? i - 1 : 0] : nbl;
         bool t = v < best;
         best = t ? v : best;
         arg = t ? l - 1 : arg;
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
         t = v < best;
         best = t ? v : best;
         arg = t ? l : arg;
-        v = fadd(bp1, wg1);
+        v = i + 1 < EPL ? nb[i + 1 < EPL ? i + 1 : 0] : nbr;
         t = v < best;
         best = t ? v : best;
         arg = t ? l + 1 : arg;
@@ -391,15 +395,15 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
 
       // ---- p row, reparametrisation (first argmin; banded values are never -0)
       store_p<EPL, FULL>(a.p + (pq_base + j - 1) * L, l0, am, nvalid);
-      uint32_t lk = order_key(out[0]);
-      int lidx = l0;
+      // lane minimum by fminf (exact: no candidate is NaN or -0, PairDesc),
+      // its first position by equality, scanning down
+      float lm = out[0];
 #pragma unroll
-      for (int i = 1; i < EPL; ++i) {
-        const uint32_t kk = order_key(out[i]);
-        const bool t = kk < lk;
-        lk = t ? kk : lk;
-        lidx = t ? l0 + i : lidx;
-      }
+      for (int i = 1; i < EPL; ++i) lm = fminf(lm, out[i]);
+      int lidx = l0 + EPL - 1;
+#pragma unroll
+      for (int i = EPL - 2; i >= 0; --i) lidx = out[i] == lm ? l0 + i : lidx;
+      const uint32_t lk = order_key(lm);
       const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
       const uint32_t qmin = __reduce_min_sync(0xffffffffu, lk == kmin ? uint32_t(lidx) : 0xffffffffu);
       const float lo = key_value(kmin);
