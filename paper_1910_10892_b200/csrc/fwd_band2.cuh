@@ -100,18 +100,45 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
     }
     const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
-    auto issue = [&](int j) {
-      const int slot = (j - 1) % ST;
-      const int prev = ld.first + (j - 1) * st;
-      const size_t off = size_t(prev) * L;
-      if (FULL || nvalid > 0) {
+    // Issue of node step j's rows into ring slot (j-1) % ST. Short rows
+    // (EPL <= 2) keep incremental state -- row pointers advanced one node
+    // step per issue, slot counters -- which cuts the per-step index
+    // arithmetic (C1 forward -9 %); at EPL >= 4 that form measured slower
+    // (C2 +2 %: the lone-warp horizontal sweeps are scheduling-sensitive), so
+    // those recompute the addresses.
+    constexpr bool kIncIssue = EPL <= 2;
+    const ptrdiff_t row_step = ptrdiff_t(st) * L;
+    if (kIncIssue) {
 #pragma unroll
-        for (int rr = 0; rr < ROWS; ++rr)
-          cp_slice_t<EPL, FULL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid);
+      for (int rr = 0; rr < ROWS; ++rr) rowp[rr] += ptrdiff_t(ld.first) * L;
+    }
+    int islot = 0, wnode_i = (r & 1) ? ld.first + st : ld.first;
+    auto issue = [&](int j) {
+      if constexpr (kIncIssue) {
+        const uint32_t sbase = ring_s + 4u * uint32_t(islot * ROWS * LS + l0);
+        if (FULL || nvalid > 0) {
+#pragma unroll
+          for (int rr = 0; rr < ROWS; ++rr) cp_slice_t<EPL, FULL>(sbase + 4u * uint32_t(rr * LS), rowp[rr], nvalid);
+        }
+        if (wpl) cp_async_u32(x_s + 4u * uint32_t(islot * 64 + lane), wrow + wnode_i, 4);
+        if (rpl) cp_async_u32(x_s + 4u * uint32_t(islot * 64 + 32 + lane), rrow + wnode_i, 4);
+#pragma unroll
+        for (int rr = 0; rr < ROWS; ++rr) rowp[rr] += row_step;
+        wnode_i += st;
+        islot = islot == ST - 1 ? 0 : islot + 1;
+      } else {
+        const int slot = (j - 1) % ST;
+        const int prev = ld.first + (j - 1) * st;
+        const size_t off = size_t(prev) * L;
+        if (FULL || nvalid > 0) {
+#pragma unroll
+          for (int rr = 0; rr < ROWS; ++rr)
+            cp_slice_t<EPL, FULL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid);
+        }
+        const int wnode = (r & 1) ? prev + st : prev;
+        if (wpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + lane), wrow + wnode, 4);
+        if (rpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + 32 + lane), rrow + wnode, 4);
       }
-      const int wnode = (r & 1) ? prev + st : prev;
-      if (wpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + lane), wrow + wnode, 4);
-      if (rpl) cp_async_u32(x_s + 4u * uint32_t(slot * 64 + 32 + lane), rrow + wnode, 4);
     };
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
@@ -124,11 +151,13 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
 #pragma unroll
     for (int i = 0; i < EPL; ++i) carry[i] = 0.0f;
 
+    int slot_c = 0;
     for (int j = 1; j <= nsteps; ++j) {
       if (j + ST - 1 <= nsteps) issue(j + ST - 1);
       cp_commit();
       cp_wait<ST - 1>();
-      const int slot = (j - 1) % ST;
+      const int slot = kIncIssue ? slot_c : (j - 1) % ST;  // ring slot of node step j
+      slot_c = slot_c == ST - 1 ? 0 : slot_c + 1;
       const float* srow = ring + slot * ROWS * LS + l0;
       if (wpl) {
         const float w = s_x[slot * 64 + lane];
