@@ -673,8 +673,16 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
       for (int i = 0; i < EPL; ++i) accl[i] = 0.0f, dtn[i] = 0.0f;
       auto load_dt = [&](int s) {
         const float* src = dthb + o_first + (nsteps - s) * stL + l0;
+        if (FULL && EPL % 2 == 0) {  // 8-byte aligned: L = 32 EPL even
 #pragma unroll
-        for (int i = 0; i < EPL; ++i) dtn[i] = (FULL || i < nvalid) ? __ldcg(src + i) : 0.0f;
+          for (int i = 0; i < EPL; i += 2) {
+            const float2 t = __ldcg(reinterpret_cast<const float2*>(src + i));
+            dtn[i] = t.x, dtn[i + 1] = t.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) dtn[i] = (FULL || i < nvalid) ? __ldcg(src + i) : 0.0f;
+        }
       };
       if (fuse && nsteps > 0) load_dt(0);
       for (int s = 0; s < nsteps; ++s) {
@@ -719,17 +727,18 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           // sums over p_l == l / |p_l - l| == 1, and sum_l g_l = 0 (the
           // reparametrised row sums to zero: dropping it changes dw only at the
           // rounding level of the reference's own sum)
+          // (predicated adds: a label feeds exactly one of the accumulators)
           float s0 = 0.0f, s1 = 0.0f;
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
             const float ga = wpl ? fmul(gg[i], w) : gg[i];  // dV addend (w folded later if constant)
             const bool cm = bit(mword, i), c0 = bit(mword, 8 + i), cp = bit(mword, 16 + i), cf = bit(mword, 24 + i);
-            vacc[i][0] = fadd(vacc[i][0], cm ? ga : 0.0f);
-            vacc[i][1] = fadd(vacc[i][1], c0 ? ga : 0.0f);
-            vacc[i][2] = fadd(vacc[i][2], cp ? ga : 0.0f);
-            fval[i] = fadd(fval[i], cf ? ga : 0.0f);
-            s0 = fadd(s0, c0 ? gg[i] : 0.0f);
-            s1 = fadd(s1, (cm || cp) ? gg[i] : 0.0f);
+            if (cm) vacc[i][0] = fadd(vacc[i][0], ga);
+            if (c0) vacc[i][1] = fadd(vacc[i][1], ga);
+            if (cp) vacc[i][2] = fadd(vacc[i][2], ga);
+            if (cf) fval[i] = fadd(fval[i], ga);
+            if (c0) s0 = fadd(s0, gg[i]);
+            if (cm || cp) s1 = fadd(s1, gg[i]);
           }
           if (do_w) wpart = fadd(fmul(fsub(gb0, gbD), s0), fmul(fsub(gb1, gbD), s1));
         } else {
