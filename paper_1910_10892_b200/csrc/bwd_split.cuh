@@ -382,6 +382,22 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
         const uint8_t* prow = reinterpret_cast<const uint8_t*>(stg + NR * LS) + (FULL ? 0 : ((size_t(e) * L) & 3)) + l0;
         const float* xs = stg + NR * LS + 8 * EPL;
         const int qv = (__float_as_uint(xs[0]) >> (8 * (e & 3))) & 0xff;
+        // fused dtheta: the running dtheta(cur) row, loaded here so the load
+        // overlaps the decode (POST then only adds the carry)
+        float dto[EPL];
+        if (fuse) {
+          const float* src = a.dtheta + size_t(b) * NL + o_first + j * stL + l0;
+          if (FULL && EPL % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < EPL; i += 2) {
+              const float2 t2 = __ldcg(reinterpret_cast<const float2*>(src + i));
+              dto[i] = t2.x, dto[i + 1] = t2.y;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < EPL; ++i) dto[i] = (FULL || i < nvalid) ? __ldcg(src + i) : 0.0f;
+          }
+        }
 #ifdef MRF_SPLIT_PROF
         const long long tc0 = clock64();
 #endif
@@ -566,7 +582,11 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
         PMARK(4);
         if (!WIN) sts_slice<EPL>(sl + SL::X + l0, x);
         sts_slice<EPL>(sl + SL::B + l0, B);
-        if (fuse) sts_slice<EPL>(sl + SL::DT + l0, rsum);
+        if (fuse) {  // dtheta_old + sum_d rho_d A[d](cur), the reference's first add
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) rsum[i] = fadd(dto[i], rsum[i]);
+          sts_slice<EPL>(sl + SL::DT + l0, rsum);
+        }
         if (!BAND) {
           uint8_t* pb = reinterpret_cast<uint8_t*>(sl + SL::P);
 #pragma unroll
@@ -668,23 +688,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
       const bool fuse = TRWP && a.dtheta != nullptr;
       float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
       float accl[EPL], rhol = 0.0f;  // last step's acc / rho (the head's own contribution)
-      float dtn[EPL];                // dtheta(cur) of the next step, loaded one step ahead
 #pragma unroll
-      for (int i = 0; i < EPL; ++i) accl[i] = 0.0f, dtn[i] = 0.0f;
-      auto load_dt = [&](int s) {
-        const float* src = dthb + o_first + (nsteps - s) * stL + l0;
-        if (FULL && EPL % 2 == 0) {  // 8-byte aligned: L = 32 EPL even
-#pragma unroll
-          for (int i = 0; i < EPL; i += 2) {
-            const float2 t = __ldcg(reinterpret_cast<const float2*>(src + i));
-            dtn[i] = t.x, dtn[i + 1] = t.y;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < EPL; ++i) dtn[i] = (FULL || i < nvalid) ? __ldcg(src + i) : 0.0f;
-        }
-      };
-      if (fuse && nsteps > 0) load_dt(0);
+      for (int i = 0; i < EPL; ++i) accl[i] = 0.0f;
       for (int s = 0; s < nsteps; ++s) {
         const uint32_t gs = gs0 + uint32_t(s);
         const int slot = int(gs % kSplitSlots);
@@ -707,8 +712,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           float dt[EPL], rs[EPL];
           lds_slice<EPL>(rs, sl + SL::DT + l0);
 #pragma unroll
-          for (int i = 0; i < EPL; ++i) dt[i] = fadd(fadd(dtn[i], rs[i]), cin[i]), accl[i] = acc[i];
-          if (s + 1 < nsteps) load_dt(s + 1);
+          for (int i = 0; i < EPL; ++i) dt[i] = fadd(rs[i], cin[i]), accl[i] = acc[i];
           stg_slice<EPL>(dthb + o_first + j * stL, l0, dt, nvalid, L);
           rhol = __uint_as_float(sc[SC_RHO]);
         }
