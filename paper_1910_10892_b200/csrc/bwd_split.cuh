@@ -222,7 +222,15 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
   const int L = g.L, N = g.N;
   const int R = RT ? RT : g.R;
   const int NR = acc_rows(TRWP, R);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifndef MRF_ROLE_ROT
+#define MRF_ROLE_ROT 3
+#endif
+  // role index: 0 = CHAIN, 1 = POST, 2.. = PRE, from the hardware warp rotated
+  // by MRF_ROLE_ROT: 3 puts CHAIN and POST on hardware warps 2 and 3 (PRE on
+  // 0, 1, 4), measured best of the five rotations (C2 backward 16.78 ->
+  // 16.12 ms, C3 17.14 -> 16.93; the rotations change which roles share a
+  // warp scheduler)
+  const int lane = threadIdx.x & 31, warp = ((threadIdx.x >> 5) + MRF_ROLE_ROT) % (2 + NPRE);
   const int stage_f = split_stage_floats(EPL, NR);
 
   float* slots = smem;                                       // [NS][SLOT]
