@@ -7,7 +7,12 @@ namespace mrf {
 template <int EPL, int R, bool FULL, bool AGG, int RD, int ST>
 static cudaError_t run_(const FwdArgs& a, int batch, cudaStream_t s) {
   constexpr int rows = 1 + (true ? R - 1 : R - 2);
-  const int wpc = warps_per_cta(a.nlines);
+  // one warp per CTA: the scheduler placement of these lone-warp chains is
+  // then the hardware's to spread (measured on C2 against 2 / 4 warps per
+  // CTA: horizontal sweeps 710 -> 690 us, vertical 531 -> 485 us; forward
+  // 12.15 -> 11.60 ms per step). The ISGMR launches (all directions at once,
+  // C1 / C3) measured better with warps_per_cta().
+  const int wpc = 1;
   const int smem = band2_smem_floats(EPL, rows, ST) * int(sizeof(float)) * wpc;
   auto kern = fwd_band2_kernel<EPL, true, R, FULL, AGG, RD, ST>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);

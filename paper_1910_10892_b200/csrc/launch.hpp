@@ -54,7 +54,11 @@ cudaError_t launch_sgm_standard(const Geometry& g, const Potentials& pot, const 
 inline bool bwd_uses_small(int L, int nlines, int batch) { return L <= 32 && int64_t(nlines) * batch >= 148 * 16; }
 
 // warps per CTA: few long chains -> spread them over every SM
-inline int warps_per_cta(int nlines) { return nlines >= 148 * 8 ? 4 : (nlines >= 148 * 2 ? 2 : 1); }
+inline int warps_per_cta(int nlines) {
+  const char* env = getenv("MRF_FWD_WPC");  // A/B: force 1, 2 or 4 warps per CTA
+  if (env && (env[0] == '1' || env[0] == '2' || env[0] == '4')) return env[0] - '0';
+  return nlines >= 148 * 8 ? 4 : (nlines >= 148 * 2 ? 2 : 1);
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
 // size) instead of on every launch (it costs host time on the launch path).
