@@ -472,12 +472,19 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
         float lsum = 0.0f;
         uint32_t mword = 0;
         int kmn = 0x7fffffff, kmx = -1;
+        if (FULL && EPL % 2 == 0) {  // the lane's p bytes, two per 16-bit load (l0 even: aligned)
+#pragma unroll
+          for (int i = 0; i < EPL; i += 2) {
+            const uint32_t v = *reinterpret_cast<const uint16_t*>(prow + i);
+            mu[i] = int(v & 0xffu), mu[i + 1] = int(v >> 8);
+          }
+        }
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
           const bool valid = FULL || i < nvalid;
           if (!valid) x[i] = 0.0f;
           lsum = fadd(lsum, x[i]);
-          mu[i] = valid ? int(prow[i]) : l0 + i;
+          if (!(FULL && EPL % 2 == 0)) mu[i] = valid ? int(prow[i]) : l0 + i;
           const int d = mu[i] - (l0 + i);
           near[i] = valid && uint32_t(d + (WIN ? kWin : 1)) <= uint32_t(WIN ? 2 * kWin : 2);
           far[i] = valid && !near[i];
