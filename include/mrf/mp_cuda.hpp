@@ -73,10 +73,13 @@ class DeviceBuffer {
   }
   size_t bytes() const { return bytes_; }
 
+  // `slack` extra bytes after the copied elements, zero-filled (p/q index
+  // buffers: the kernels read them as aligned 32-bit words)
   template <class T>
-  static DeviceBuffer upload(const T* src, size_t count) {
-    DeviceBuffer b(sizeof(T) * count);
+  static DeviceBuffer upload(const T* src, size_t count, size_t slack = 0) {
+    DeviceBuffer b(sizeof(T) * count + slack);
     if (count) check_cuda(cudaMemcpy(b.ptr_, src, sizeof(T) * count, cudaMemcpyHostToDevice), "H2D");
+    if (slack) check_cuda(cudaMemset(static_cast<char*>(b.ptr_) + sizeof(T) * count, 0, slack), "memset");
     return b;
   }
   template <class T>
@@ -334,8 +337,11 @@ struct PotentialSet {
 class IndexStore {
  public:
   IndexStore(const GridTopology& topo, int labels) : labels_(labels), edges_(topo.total_edges()) {}
-  void append_iteration() {
-    ++iterations_;
+  void append_iteration() { set_iterations(iterations_ + 1); }
+  // not in the reference: size the store for k iterations at once (the
+  // device path fills every iteration in one copy)
+  void set_iterations(int k) {
+    iterations_ = k;
     p_.resize(size_t(iterations_) * edges_ * labels_, 0);
     q_.resize(size_t(iterations_) * edges_, 0);
   }
@@ -470,6 +476,7 @@ inline ForwardResult<float> forward(int engine, const GridTopology& topo, const 
     throw std::invalid_argument(engine == MRF_ENGINE_ISGMR ? "isgmr_forward: iterations must be >= 1"
                                                            : "trwp_forward: iterations must be >= 1");
   DeviceProblem d = upload(topo, pots, rho, true);
+  d.prob.assume_finite = 1;  // checked on the host above
   const int L = d.prob.labels, R = topo.num_dirs();
   const size_t n = size_t(topo.grid().nodes()), E = size_t(topo.total_edges());
   DeviceBuffer cost(sizeof(float) * n * L), labels(2 * n), msg(sizeof(float) * R * n * L), p(size_t(K) * E * L + 4),
@@ -488,7 +495,7 @@ inline ForwardResult<float> forward(int engine, const GridTopology& topo, const 
   res.output.cost.resize(n * L);
   res.output.labels_map.resize(n);
   res.messages.resize(size_t(R) * n * L);
-  for (int k = 0; k < K; ++k) res.indices.append_iteration();
+  res.indices.set_iterations(K);
   cost.download(res.output.cost.data(), n * L);
   labels.download(res.output.labels_map.data(), n);
   msg.download(res.messages.data(), res.messages.size());
@@ -507,8 +514,8 @@ inline GradientSet<float> backward(int engine, const GridTopology& topo, const P
     throw std::invalid_argument("backward: index store does not match the problem");
   const int K = indices.iterations();
   DeviceProblem d = upload(topo, pots, rho, false);
-  DeviceBuffer p = DeviceBuffer::upload(indices.p_data().data(), indices.p_data().size() + 4);
-  DeviceBuffer q = DeviceBuffer::upload(indices.q_data().data(), indices.q_data().size() + 4);
+  DeviceBuffer p = DeviceBuffer::upload(indices.p_data().data(), indices.p_data().size(), 4);
+  DeviceBuffer q = DeviceBuffer::upload(indices.q_data().data(), indices.q_data().size(), 4);
   DeviceBuffer gc = DeviceBuffer::upload(grad_cost.data(), grad_cost.size());
   DeviceBuffer gu(sizeof(float) * n * L), gv(sizeof(float) * L * L), gw(sizeof(float) * (R / 2) * n);
   const size_t wsb = mrf_backward_workspace_bytes(topo.handle(), &d.prob, engine, K);
@@ -571,6 +578,185 @@ GradientSet<Real> trwp_backward(const GridTopology& topo, const PotentialSet<Rea
   (void)threads;
   return cuda_detail::backward(MRF_ENGINE_TRWP, topo, pots, &rho, indices, grad_cost);
 }
+
+namespace cuda_detail {
+
+// Device state of one IsgmrEngine / TrwpEngine: the potentials uploaded once,
+// messages (ISGMR: published m and swept mhat), and the index store on the
+// device, grown by doubling when step() runs past its capacity (the
+// reference's append_iteration regrows the host vectors every iteration,
+// index_store.hpp:21-25). Host copies are made on demand.
+class EngineState {
+ public:
+  EngineState(int engine, const GridTopology& topo, const PotentialSet<float>& pots, const TreeCoefficients<float>* rho,
+              bool diagnostic)
+      : engine_(engine), topo_(topo), d_(upload(topo, pots, rho, true)) {
+    d_.prob.assume_finite = 1;  // checked on the host by upload()
+    L_ = d_.prob.labels;
+    R_ = topo.num_dirs();
+    n_ = size_t(topo.grid().nodes());
+    E_ = size_t(topo.total_edges());
+    const size_t mb = sizeof(float) * R_ * n_ * L_;
+    m_ = DeviceBuffer(mb);
+    check_cuda(cudaMemset(m_.as<void>(), 0, mb), "memset");
+    if (engine == MRF_ENGINE_ISGMR) {
+      mhat_ = DeviceBuffer(mb);
+      check_cuda(cudaMemset(mhat_.as<void>(), 0, mb), "memset");
+    }
+    reserve(1);
+    if (diagnostic) {
+      const float inf = std::numeric_limits<float>::infinity();
+      gap_ = DeviceBuffer::upload(&inf, 1);
+      d_.prob.diag_gap = gap_.as<float>();
+    }
+  }
+
+  void step() {
+    if (k_ == cap_) reserve(2 * cap_);
+    if (engine_ == MRF_ENGINE_ISGMR) {
+      check(mrf_isgmr_step_f32(topo_.handle(), &d_.prob, k_, cap_, m_.as<float>(), mhat_.as<float>(),
+                               p_.as<std::uint8_t>(), q_.as<std::uint8_t>(), nullptr));
+      std::swap(m_, mhat_);  // publish m <- mhat (isgmr.hpp:55)
+    } else {
+      check(mrf_trwp_step_f32(topo_.handle(), &d_.prob, k_, cap_, m_.as<float>(), p_.as<std::uint8_t>(),
+                              q_.as<std::uint8_t>(), nullptr));
+    }
+    ++k_;
+  }
+
+  int iterations() const { return k_; }
+
+  CostOutput<float> aggregate() const {
+    DeviceBuffer cost(sizeof(float) * n_ * L_), labels(2 * n_);
+    check(mrf_aggregate_f32(topo_.handle(), &d_.prob, m_.as<float>(), cost.as<float>(), labels.as<std::uint16_t>(),
+                            nullptr));
+    CostOutput<float> out;
+    out.height = topo_.grid().height;
+    out.width = topo_.grid().width;
+    out.labels = L_;
+    out.cost.resize(n_ * L_);
+    out.labels_map.resize(n_);
+    cost.download(out.cost.data(), out.cost.size());
+    labels.download(out.labels_map.data(), n_);
+    return out;
+  }
+
+  void messages(std::vector<float>& out) const {
+    out.resize(size_t(R_) * n_ * L_);
+    m_.download(out.data(), out.size());
+  }
+
+  IndexStore indices() const {
+    IndexStore st(topo_, L_);
+    st.set_iterations(k_);
+    p_.download(st.p_data().data(), st.p_data().size());
+    q_.download(st.q_data().data(), st.q_data().size());
+    return st;
+  }
+
+  float gap() const {
+    float g = std::numeric_limits<float>::infinity();
+    if (gap_.bytes()) gap_.download(&g, 1);
+    return g;
+  }
+
+ private:
+  void reserve(int cap) {
+    // +4 bytes: the kernels read p/q as aligned 32-bit words
+    DeviceBuffer p(size_t(cap) * E_ * L_ + 4), q(size_t(cap) * E_ + 4);
+    if (k_) {
+      check_cuda(cudaMemcpy(p.as<void>(), p_.as<void>(), size_t(k_) * E_ * L_, cudaMemcpyDeviceToDevice), "D2D");
+      check_cuda(cudaMemcpy(q.as<void>(), q_.as<void>(), size_t(k_) * E_, cudaMemcpyDeviceToDevice), "D2D");
+    }
+    p_ = std::move(p);
+    q_ = std::move(q);
+    cap_ = cap;
+  }
+
+  int engine_;
+  const GridTopology& topo_;
+  DeviceProblem d_;
+  int L_ = 0, R_ = 0;
+  size_t n_ = 0, E_ = 0;
+  int k_ = 0, cap_ = 0;
+  DeviceBuffer m_, mhat_, p_, q_, gap_;
+};
+
+}  // namespace cuda_detail
+
+/// isgmr.hpp:26-143. Same interface; the potentials are uploaded at
+/// construction (the reference keeps references to them), every step() runs
+/// on the device and host copies are made by messages() / indices() /
+/// aggregate(). `diagnostic` (not in the reference) turns on min_argmin_gap
+/// tracking (dense min-plus kernel: same results, slower); without it
+/// min_argmin_gap() is +inf.
+template <class Real>
+class IsgmrEngine {
+ public:
+  IsgmrEngine(const GridTopology& topo, const PotentialSet<Real>& pots, int threads = 1, bool diagnostic = false)
+      : st_((cuda_detail::require_float<Real>(), MRF_ENGINE_ISGMR), topo, pots, nullptr, diagnostic) {
+    (void)threads;
+  }
+  void step() { st_.step(); }
+  int iterations() const { return st_.iterations(); }
+  CostOutput<Real> aggregate() const { return st_.aggregate(); }
+  const std::vector<Real>& messages() const {
+    st_.messages(m_);
+    return m_;
+  }
+  const IndexStore& indices() const {
+    idx_.emplace(st_.indices());
+    return *idx_;
+  }
+  IndexStore&& take_indices() {
+    idx_.emplace(st_.indices());
+    return std::move(*idx_);
+  }
+  Real min_argmin_gap() const { return st_.gap(); }
+
+ private:
+  cuda_detail::EngineState st_;
+  mutable std::vector<Real> m_;
+  mutable std::optional<IndexStore> idx_;
+};
+
+/// trwp.hpp:25-146 (see IsgmrEngine).
+template <class Real>
+class TrwpEngine {
+ public:
+  TrwpEngine(const GridTopology& topo, const PotentialSet<Real>& pots, TreeCoefficients<Real> rho, int threads = 1,
+             bool diagnostic = false)
+      : rho_(check_rho(std::move(rho))), st_(MRF_ENGINE_TRWP, topo, pots, &rho_, diagnostic) {
+    (void)threads;
+  }
+  void step() { st_.step(); }
+  int iterations() const { return st_.iterations(); }
+  CostOutput<Real> aggregate() const { return st_.aggregate(); }
+  const std::vector<Real>& messages() const {
+    st_.messages(m_);
+    return m_;
+  }
+  const IndexStore& indices() const {
+    idx_.emplace(st_.indices());
+    return *idx_;
+  }
+  IndexStore&& take_indices() {
+    idx_.emplace(st_.indices());
+    return std::move(*idx_);
+  }
+  Real min_argmin_gap() const { return st_.gap(); }
+
+ private:
+  static TreeCoefficients<Real> check_rho(TreeCoefficients<Real> rho) {
+    cuda_detail::require_float<Real>();
+    if (rho.planes.empty() && !(rho.uniform > 0 && rho.uniform <= 1)) throw std::invalid_argument("rho must be in (0, 1]");
+    return rho;
+  }
+  TreeCoefficients<Real> rho_;
+  cuda_detail::EngineState st_;
+  mutable std::vector<Real> m_;
+  mutable std::optional<IndexStore> idx_;
+};
 
 /// softhead.hpp:15-20
 template <class Real>
@@ -648,6 +834,39 @@ double energy(const GridTopology& topo, const PotentialSet<Real>& pots, const st
   double e = 0.0;
   cuda_detail::check(mrf_energy_f32(topo.handle(), &d.prob, dl.as<std::uint16_t>(), &e, nullptr));
   return e;
+}
+
+/// isgmr.hpp:156-169: energy of the aggregated labelling after each
+/// iteration, optionally on a separate evaluation topology (the 4-connected
+/// protocol).
+template <class Real>
+std::vector<double> isgmr_iterate_energy(const GridTopology& topo, const PotentialSet<Real>& pots, int iterations,
+                                         int threads = 1, const GridTopology* eval_topo = nullptr) {
+  const GridTopology& et = eval_topo ? *eval_topo : topo;
+  IsgmrEngine<Real> engine(topo, pots, threads);
+  std::vector<double> energies;
+  energies.reserve(iterations > 0 ? iterations : 0);
+  for (int k = 0; k < iterations; ++k) {
+    engine.step();
+    energies.push_back(energy(et, pots, engine.aggregate().labels_map));
+  }
+  return energies;
+}
+
+/// trwp.hpp:158-171
+template <class Real>
+std::vector<double> trwp_iterate_energy(const GridTopology& topo, const PotentialSet<Real>& pots,
+                                        const TreeCoefficients<Real>& rho, int iterations, int threads = 1,
+                                        const GridTopology* eval_topo = nullptr) {
+  const GridTopology& et = eval_topo ? *eval_topo : topo;
+  TrwpEngine<Real> engine(topo, pots, rho, threads);
+  std::vector<double> energies;
+  energies.reserve(iterations > 0 ? iterations : 0);
+  for (int k = 0; k < iterations; ++k) {
+    engine.step();
+    energies.push_back(energy(et, pots, engine.aggregate().labels_map));
+  }
+  return energies;
 }
 
 }  // namespace mp

@@ -33,7 +33,11 @@
  *    queries; it needs no initialisation.
  *  - Results are bit-identical to the reference CPU implementation for
  *    messages, cost, labels, p and q (FP32, no FMA contraction, lowest index
- *    wins ties), and deterministic run to run for the gradients.
+ *    wins ties). Gradients match within 1e-5 (normwise and elementwise) and
+ *    are bit-identical run to run.
+ *  - p and q buffers are read as aligned 32-bit words: their allocations must
+ *    extend to the next multiple of 4 bytes past the last index byte (any
+ *    cudaMalloc allocation does; a sub-buffer needs up to 3 bytes of slack).
  */
 #ifndef MRF_CUDA_H
 #define MRF_CUDA_H
@@ -90,6 +94,19 @@ typedef struct {
   const float* weight_planes;/* [B][R/2][N] or NULL */
   float rho;                 /* TRWP uniform tree coefficient (0,1], used when rho_planes == NULL */
   const float* rho_planes;   /* [B][R/2][N] or NULL */
+  /* 0 (default): the forward entry points scan `unary` for non-finite values
+   * and return MRF_EINVAL (the reference engines throw, isgmr.hpp:32-35,
+   * trwp.hpp:33-36); this synchronises `stream` once per call. 1: the caller
+   * guarantees finite unaries (no scan). */
+  int assume_finite;
+  /* NULL (default), or device float [B] initialised by the caller (e.g. to
+   * +inf): diagnostic mode. Every forward sweep then also tracks the smallest
+   * (second best - best) gap of the min-plus argmins and of the
+   * reparametrisation argmin (IsgmrEngine/TrwpEngine::min_argmin_gap,
+   * isgmr.hpp:64-68,109-115,125-129, trwp.hpp:57-59) and min-accumulates it
+   * into diag_gap[b]. Diagnostic sweeps run the dense min-plus kernel (every
+   * (mu, l) candidate): same messages and indices, much slower. */
+  float* diag_gap;
 } mrf_problem_f32;
 
 typedef struct {

@@ -207,6 +207,7 @@ class Forward:
     messages: np.ndarray
     p: np.ndarray
     q: np.ndarray
+    gap: float = float("inf")  # ForwardResult::min_argmin_gap (impl="ref" only)
 
 
 @dataclass
@@ -255,6 +256,7 @@ def forward(engine: str, pr: Problem, K: int, impl: str = "oracle", threads: int
                                                 _ptr(pr.w_planes), pr.rho_const, _ptr(pr.rho_planes), K, threads,
                                                 _ptr(out.cost), _ptr(out.labels), _ptr(out.messages), _ptr(out.p),
                                                 _ptr(out.q), _ptr(gap)))
+        out.gap = float(gap[0])
     return out
 
 

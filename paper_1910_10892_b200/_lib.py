@@ -29,7 +29,8 @@ class MrfInvalidArgument(MrfError, ValueError):
 class Problem(C.Structure):
     _fields_ = [("batch", C.c_int), ("height", C.c_int), ("width", C.c_int), ("labels", C.c_int),
                 ("unary", C.c_void_p), ("pairwise", C.c_void_p), ("weight", C.c_float),
-                ("weight_planes", C.c_void_p), ("rho", C.c_float), ("rho_planes", C.c_void_p)]
+                ("weight_planes", C.c_void_p), ("rho", C.c_float), ("rho_planes", C.c_void_p),
+                ("assume_finite", C.c_int), ("diag_gap", C.c_void_p)]
 
 
 class ForwardOut(C.Structure):

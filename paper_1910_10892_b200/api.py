@@ -96,6 +96,8 @@ class MRF:
     V       [L, L]    float32 cuda       (PairwiseFunction::table)
     weight  float, or [B, R/2, N] tensor (EdgeWeights constant / planes)
     rho     float, or [B, R/2, N] tensor (TreeCoefficients, TRWP only)
+    assume_finite  skip the forward's non-finite unary scan (the reference
+                   engines throw on non-finite unaries; default: scan)
     """
 
     topo: GridTopology
@@ -103,6 +105,7 @@ class MRF:
     V: torch.Tensor
     weight: float | torch.Tensor = 1.0
     rho: float | torch.Tensor = 0.5
+    assume_finite: bool = False
 
     def __post_init__(self):
         t = self.topo
@@ -135,13 +138,14 @@ class MRF:
     def labels(self):
         return self.unary.shape[2]
 
-    def c_problem(self) -> _lib.Problem:
+    def c_problem(self, diag_gap: torch.Tensor | None = None) -> _lib.Problem:
         t = self.topo
         wt = self.weight if isinstance(self.weight, torch.Tensor) else None
         rt = self.rho if isinstance(self.rho, torch.Tensor) else None
         return _lib.Problem(self.batch, t.height, t.width, self.labels, self.unary.data_ptr(), self.V.data_ptr(),
                             0.0 if wt is not None else float(self.weight), None if wt is None else wt.data_ptr(),
-                            0.5 if rt is not None else float(self.rho), None if rt is None else rt.data_ptr())
+                            0.5 if rt is not None else float(self.rho), None if rt is None else rt.data_ptr(),
+                            int(self.assume_finite), None if diag_gap is None else diag_gap.data_ptr())
 
 
 @dataclass
@@ -156,6 +160,8 @@ class ForwardResult:
     p: torch.Tensor
     q: torch.Tensor
     iterations: int
+    # [B] (diagnostic=True) or None: the reference's min_argmin_gap (+inf when untracked)
+    min_argmin_gap: torch.Tensor | None = None
 
 
 @dataclass
@@ -201,11 +207,15 @@ def _workspace(kind: str, nbytes: int, device, stream):
     return buf
 
 
-def _forward(engine: int, mrf: MRF, K: int, out: ForwardResult | None, stream):
+def _forward(engine: int, mrf: MRF, K: int, out: ForwardResult | None, stream, diagnostic: bool = False):
     if K < 1:
         raise _lib.MrfInvalidArgument(1, "iterations must be >= 1")
     out = out or _alloc_forward(mrf, K)
-    pr = mrf.c_problem()
+    gap = None
+    if diagnostic:
+        gap = torch.full((mrf.batch,), float("inf"), dtype=torch.float32, device=mrf.unary.device)
+    out.min_argmin_gap = gap
+    pr = mrf.c_problem(gap)
     wsb = lib().mrf_forward_workspace_bytes(mrf.topo.handle, C.byref(pr), engine, K)
     ws = _workspace("fwd", wsb, mrf.unary.device, stream)
     fo = _lib.ForwardOut(_ptr(out.cost), _ptr(out.labels), _ptr(out.messages), _ptr(out.p), _ptr(out.q))
@@ -214,14 +224,17 @@ def _forward(engine: int, mrf: MRF, K: int, out: ForwardResult | None, stream):
     return out
 
 
-def isgmr_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None) -> ForwardResult:
-    """mp::isgmr_forward<float> (isgmr.hpp:145-152) for a batch."""
-    return _forward(ENGINE_ISGMR, mrf, iterations, out, stream)
+def isgmr_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None,
+                  diagnostic: bool = False) -> ForwardResult:
+    """mp::isgmr_forward<float> (isgmr.hpp:145-152) for a batch. diagnostic=True
+    also tracks min_argmin_gap (dense kernel: same results, slower)."""
+    return _forward(ENGINE_ISGMR, mrf, iterations, out, stream, diagnostic)
 
 
-def trwp_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None) -> ForwardResult:
+def trwp_forward(mrf: MRF, iterations: int, out: ForwardResult | None = None, stream=None,
+                 diagnostic: bool = False) -> ForwardResult:
     """mp::trwp_forward<float> (trwp.hpp:148-156) for a batch; rho from mrf.rho."""
-    return _forward(ENGINE_TRWP, mrf, iterations, out, stream)
+    return _forward(ENGINE_TRWP, mrf, iterations, out, stream, diagnostic)
 
 
 def _backward(engine: int, mrf: MRF, fwd_p, fwd_q, K: int, grad_cost, out: GradientSet | None, stream):
@@ -263,24 +276,65 @@ def aggregate(mrf: MRF, messages, cost=None, labels=None, stream=None):
     return cost, labels
 
 
-class IsgmrEngine:
-    """mp::IsgmrEngine (isgmr.hpp:26-143): step() runs one iteration,
-    aggregate() returns (cost, labels). Index capacity is fixed up front."""
+class _Engine:
+    """Shared state of the engine classes: messages on the device, indices
+    in a [B, K_cap, E, L] / [B, K_cap, E] store that grows by doubling when
+    step() runs past its capacity (the reference regrows on every
+    append_iteration, index_store.hpp:21-25)."""
 
-    def __init__(self, mrf: MRF, max_iterations: int):
+    def __init__(self, mrf: MRF, max_iterations: int, diagnostic: bool):
+        if mrf.labels > 256:
+            raise _lib.MrfInvalidArgument(1, "engine: more than 256 labels")
+        if not mrf.assume_finite and not check_finite(mrf.unary):
+            raise _lib.MrfInvalidArgument(1, "engine: non-finite unary potential")
+        t, dev = mrf.topo, mrf.unary.device
+        self.mrf, self.k = mrf, 0
+        self.K_cap = max(1, max_iterations)
+        self.p = torch.empty((mrf.batch, self.K_cap, t.total_edges, mrf.labels), dtype=torch.uint8, device=dev)
+        self.q = torch.empty((mrf.batch, self.K_cap, t.total_edges), dtype=torch.uint8, device=dev)
+        self.gap = torch.full((mrf.batch,), float("inf"), dtype=torch.float32, device=dev) if diagnostic else None
+
+    def _reserve(self):
+        if self.k < self.K_cap:
+            return
+        cap = 2 * self.K_cap
+        p = torch.empty((self.p.shape[0], cap) + tuple(self.p.shape[2:]), dtype=torch.uint8, device=self.p.device)
+        q = torch.empty((self.q.shape[0], cap, self.q.shape[2]), dtype=torch.uint8, device=self.q.device)
+        p[:, :self.K_cap].copy_(self.p)
+        q[:, :self.K_cap].copy_(self.q)
+        self.p, self.q, self.K_cap = p, q, cap
+
+    def iterations(self):
+        return self.k
+
+    def indices(self):
+        """(p, q) of the iterations run so far: [B, k, E, L], [B, k, E]."""
+        return self.p[:, :self.k], self.q[:, :self.k]
+
+    def aggregate(self, stream=None):
+        return aggregate(self.mrf, self.messages(), stream=stream)
+
+    def min_argmin_gap(self):
+        """[B] floats in diagnostic mode, else +inf (not tracked)."""
+        if self.gap is None:
+            return torch.full((self.mrf.batch,), float("inf"))
+        return self.gap.cpu()
+
+
+class IsgmrEngine(_Engine):
+    """mp::IsgmrEngine (isgmr.hpp:26-143): step() runs one iteration,
+    aggregate() returns (cost, labels)."""
+
+    def __init__(self, mrf: MRF, max_iterations: int = 1, diagnostic: bool = False):
+        super().__init__(mrf, max_iterations, diagnostic)
         t = mrf.topo
-        self.mrf, self.K_cap, self.k = mrf, max_iterations, 0
         shape = (mrf.batch, t.num_dirs, t.nodes, mrf.labels)
         self.m = torch.zeros(shape, dtype=torch.float32, device=mrf.unary.device)
         self.mhat = torch.zeros(shape, dtype=torch.float32, device=mrf.unary.device)
-        self.p = torch.empty((mrf.batch, max_iterations, t.total_edges, mrf.labels), dtype=torch.uint8,
-                             device=mrf.unary.device)
-        self.q = torch.empty((mrf.batch, max_iterations, t.total_edges), dtype=torch.uint8, device=mrf.unary.device)
 
     def step(self, stream=None):
-        if self.k >= self.K_cap:
-            raise _lib.MrfInvalidArgument(1, "index store capacity exhausted")
-        pr = self.mrf.c_problem()
+        self._reserve()
+        pr = self.mrf.c_problem(self.gap)
         check(lib().mrf_isgmr_step_f32(self.mrf.topo.handle, C.byref(pr), self.k, self.K_cap, _ptr(self.m),
                                        _ptr(self.mhat), _ptr(self.p), _ptr(self.q), _stream(stream)))
         self.m, self.mhat = self.mhat, self.m  # publish m <- mhat (isgmr.hpp:55)
@@ -289,35 +343,27 @@ class IsgmrEngine:
     def messages(self):
         return self.m
 
-    def aggregate(self, stream=None):
-        return aggregate(self.mrf, self.m, stream=stream)
 
-
-class TrwpEngine:
+class TrwpEngine(_Engine):
     """mp::TrwpEngine (trwp.hpp:25-146)."""
 
-    def __init__(self, mrf: MRF, max_iterations: int):
+    def __init__(self, mrf: MRF, max_iterations: int = 1, diagnostic: bool = False):
+        super().__init__(mrf, max_iterations, diagnostic)
         t = mrf.topo
-        self.mrf, self.K_cap, self.k = mrf, max_iterations, 0
+        if not isinstance(mrf.rho, torch.Tensor) and not (0.0 < float(mrf.rho) <= 1.0):
+            raise _lib.MrfInvalidArgument(1, "rho must be in (0, 1]")
         self.m = torch.zeros((mrf.batch, t.num_dirs, t.nodes, mrf.labels), dtype=torch.float32,
                              device=mrf.unary.device)
-        self.p = torch.empty((mrf.batch, max_iterations, t.total_edges, mrf.labels), dtype=torch.uint8,
-                             device=mrf.unary.device)
-        self.q = torch.empty((mrf.batch, max_iterations, t.total_edges), dtype=torch.uint8, device=mrf.unary.device)
 
     def step(self, stream=None):
-        if self.k >= self.K_cap:
-            raise _lib.MrfInvalidArgument(1, "index store capacity exhausted")
-        pr = self.mrf.c_problem()
+        self._reserve()
+        pr = self.mrf.c_problem(self.gap)
         check(lib().mrf_trwp_step_f32(self.mrf.topo.handle, C.byref(pr), self.k, self.K_cap, _ptr(self.m),
                                       _ptr(self.p), _ptr(self.q), _stream(stream)))
         self.k += 1
 
     def messages(self):
         return self.m
-
-    def aggregate(self, stream=None):
-        return aggregate(self.mrf, self.m, stream=stream)
 
 
 def check_finite(x: torch.Tensor, stream=None) -> bool:

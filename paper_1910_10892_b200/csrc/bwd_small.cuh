@@ -54,8 +54,8 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
   const float* dcb = a.dc + size_t(b) * NL + lane;
   const float* ainb = a.ain + size_t(b) * R * NL + lane;
   float* aoutb = a.aout + size_t(b) * R * NL + lane;
-  const uint8_t* pimg = a.p + size_t(b) * g.K_cap * g.E * L;
-  const uint8_t* qimg = a.q + size_t(b) * g.K_cap * g.E;
+  const uint8_t* pimg = a.p;
+  const uint8_t* qimg = a.q;
   const int warp_global = blockIdx.x * wpc + wid;
   for (int t = lane; t < 32 * 32; t += 32) s_dv[t] = 0.0f;
   int v_orient = -1;
@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     const int npl = nrows;  // plane rows end here
     const bool fuse = TRWP && a.dtheta != nullptr;
     float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
-    const uint32_t ebase = uint32_t(a.k) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
+    // edge index over the whole batch: p/q words are addressed from a.p/a.q so
+    // that byte offsets stay word-aligned for any b, K_cap and E (K*E odd)
+    const uint32_t ebase = (uint32_t(b) * uint32_t(g.K_cap) + uint32_t(a.k)) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
     const float* rowb[NRMAX];  // this lane's element of each staged row, at node 0
 #pragma unroll
     for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] = sd[rr] < 0 ? dcb : ainb + size_t(sd[rr] > 0 ? sd[rr] : 0) * NL;

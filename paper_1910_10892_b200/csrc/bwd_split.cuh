@@ -279,7 +279,9 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
     const int nsteps = ld.length - 1;
     const int stL = st * L;
     const int o_first = ld.first * L;
-    const uint32_t ebase = uint32_t(a.k) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
+    // edge index over the whole batch: p/q words are addressed from a.p/a.q so
+    // that byte offsets stay word-aligned for any b, K_cap and E (K*E odd)
+    const uint32_t ebase = (uint32_t(b) * uint32_t(g.K_cap) + uint32_t(a.k)) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
 
     if (warp >= 2) {
       // =============================== PRE ===============================
@@ -288,8 +290,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
       const uint32_t ring_s = smem_u32(ring);
       const float* dcb = a.dc + size_t(b) * NL;
       const float* ainb = a.ain + size_t(b) * R * NL;
-      const uint8_t* pimg = a.p + size_t(b) * g.K_cap * g.E * L;
-      const uint8_t* qimg = a.q + size_t(b) * g.K_cap * g.E;
+      const uint8_t* pimg = a.p;
+      const uint8_t* qimg = a.q;
       const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
       const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
       // the rows gm^r(cur) is assembled from, in accumulation order (-1 = dc)

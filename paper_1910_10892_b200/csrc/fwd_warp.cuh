@@ -98,6 +98,9 @@ struct FwdArgs {
   float* agg_cost;
   uint16_t* agg_labels;
   int dir;  // the one direction every line of the launch sweeps (TRWP), -1: mixed (ISGMR)
+  // diagnostic mode (mrf_problem_f32::diag_gap): [B] floats min-accumulating
+  // the (second best - best) argmin gaps; only fwd_warp_kernel is launched
+  float* diag_gap;
 };
 
 __device__ __forceinline__ void cp_async_u32(uint32_t saddr, const void* gmem, int bytes) {
@@ -213,7 +216,16 @@ __host__ __device__ constexpr int fwd_warp_smem_floats(int EPL, int rows) {
   return ((kStages * rows + 3) * 32 * EPL + kStages * 64 + (2 * 32 * EPL + 3) / 4 + 256 + 31) / 32 * 32;
 }
 
-template <int EPL, bool TRWP, int MODE>
+// min over gaps with the reference's `if (g < gap) gap = g` (NaN never wins)
+__device__ __forceinline__ void gap_min(float& gap, float g) {
+  if (g < gap) gap = g;
+}
+
+// MODE 0 dense, 1 banded (shared memory), 2 banded D == 2 (shuffles). GAP
+// (MODE 0 only): also track min_argmin_gap the way the reference's sweep
+// does (isgmr.hpp:100-116,119-129: second best per label and for the
+// reparametrisation argmin) and atomically min it into a.diag_gap[b].
+template <int EPL, bool TRWP, int MODE, bool GAP = false>
 __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
   const Geometry& g = a.g;
   const int L = g.L, N = g.N, R = g.R;
@@ -251,6 +263,7 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
     for (int d = lane; d <= D && d < 256; d += 32) s_wg[d] = fmul(a.pot.w, gt[d]);
     __syncwarp();
   }
+  float gap = kInf;  // GAP: this lane's running minimum
 
   for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
     const LineDesc ld = a.lines[li];
@@ -340,6 +353,9 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
 
       float out[EPL];
       int arg[EPL];
+      float sec[EPL];  // GAP: second best candidate per label
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) sec[i] = kInf;
       if (MODE != 0) {
         float c;
         if (MODE == 2) {
@@ -496,7 +512,12 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
           for (int mu = 0; mu < 32; ++mu) {
             if (mu < L) {
               const float v = fadd(s_base[mu], fmul(w, vcol[mu < 32 ? mu : 0]));
-              if (v < out[0]) out[0] = v, arg[0] = mu;
+              if (GAP) {
+                if (v < out[0]) sec[0] = out[0], out[0] = v, arg[0] = mu;
+                else if (v < sec[0]) sec[0] = v;
+              } else if (v < out[0]) {
+                out[0] = v, arg[0] = mu;
+              }
             }
           }
         } else {
@@ -507,7 +528,12 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
               const int l = l0 + i < L ? l0 + i : 0;
               const float vv = __ldg(a.pot.V + ((r & 1) ? size_t(l) * L + mu : size_t(mu) * L + l));
               const float v = fadd(bm, fmul(w, vv));
-              if (v < out[i]) out[i] = v, arg[i] = mu;
+              if (GAP) {
+                if (v < out[i]) sec[i] = out[i], out[i] = v, arg[i] = mu;
+                else if (v < sec[i]) sec[i] = v;
+              } else if (v < out[i]) {
+                out[i] = v, arg[i] = mu;
+              }
             }
           }
         }
@@ -529,6 +555,21 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
       const uint32_t tmin = __reduce_min_sync(0xffffffffu, lk == kmin ? lt : 0xffffffffu);
       float lo = key_value(kmin);
       if (tmin & 1u) lo = -0.0f;
+      if (GAP) {
+        // second smallest message entry = min over l != lstar (ties included)
+        const int lstar = int(tmin >> 1);
+        uint32_t sk = 0xffffffffu;
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+          if (i < nvalid) {
+            gap_min(gap, fsub(sec[i], out[i]));
+            if (l0 + i != lstar) sk = min(sk, order_key(fadd(out[i], 0.0f)));
+          }
+        }
+        const uint32_t skm = __reduce_min_sync(0xffffffffu, sk);
+        const float second = skm == 0xffffffffu ? kInf : key_value(skm);
+        gap_min(gap, fsub(second, lo));
+      }
 #pragma unroll
       for (int i = 0; i < EPL; ++i) carry[i] = fsub(out[i], lo);
       stg_slice<EPL>(a.m_out + img + (size_t(r) * N + cur) * L, l0, carry, nvalid, L);
@@ -538,6 +579,13 @@ __device__ __forceinline__ void fwd_sweep_lines(const FwdArgs& a, float* ws) {
     cp_wait<0>();
     __syncwarp();
   }
+  if (GAP) {
+    // gaps are >= 0 (or -0, or +inf): their int bits order like the values
+    int gi = __float_as_int(gap);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) gi = min(gi, __shfl_xor_sync(0xffffffffu, gi, off));
+    if (lane == 0 && gi != __float_as_int(kInf)) atomicMin(reinterpret_cast<int*>(a.diag_gap) + b, gi);
+  }
 }
 
 template <int EPL, bool TRWP>
@@ -546,6 +594,10 @@ __global__ void __launch_bounds__(128) fwd_warp_kernel(FwdArgs a) {
   const int R = a.g.R;
   const int rows = 1 + (TRWP ? R - 1 : R - 2);
   float* ws = smem + size_t(threadIdx.x >> 5) * fwd_warp_smem_floats(EPL, rows);
+  if (a.diag_gap) {  // diagnostic mode: the only kernel launched for the sweep
+    fwd_sweep_lines<EPL, TRWP, 0, true>(a, ws);
+    return;
+  }
   if (a.desc->banded) {
     if (a.desc->D == 2) {
       if (!a.band2_launched) fwd_sweep_lines<EPL, TRWP, 2>(a, ws);

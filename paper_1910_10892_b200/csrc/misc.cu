@@ -2,6 +2,7 @@
 // data-parallel collective (NCCL all-reduce, resolved at run time).
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include <cstdio>
@@ -39,14 +40,21 @@ cudaError_t ensure_dynamic_smem(const void* kern, int bytes) {
 
 namespace {
 
+// Clears *flag when any of x[0:n] is Inf or NaN (exponent all ones). 16-byte
+// loads for the aligned bulk; every thread folds its words, one vote per warp.
 __global__ void finite_kernel(const float* __restrict__ x, size_t n, int* flag) {
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-    const uint32_t u = __float_as_uint(x[i]);
-    if ((u & 0x7f800000u) == 0x7f800000u) {
-      *flag = 0;
-      return;
-    }
+  const size_t tid = size_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = size_t(gridDim.x) * blockDim.x;
+  const size_t head = (reinterpret_cast<uintptr_t>(x) & 15u) ? n : 0;  // unaligned: scalar only
+  const size_t nv = (n - head) / 4;
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  uint32_t bad = 0;
+  for (size_t i = tid; i < nv; i += nth) {
+    const uint4 v = __ldcs(xv + i);
+    bad |= ((v.x & 0x7f800000u) == 0x7f800000u) | ((v.y & 0x7f800000u) == 0x7f800000u) |
+           ((v.z & 0x7f800000u) == 0x7f800000u) | ((v.w & 0x7f800000u) == 0x7f800000u);
   }
+  for (size_t i = 4 * nv + tid; i < n; i += nth) bad |= (__float_as_uint(x[i]) & 0x7f800000u) == 0x7f800000u;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0;
 }
 
 // out[0:L*L] = sum_b pairwise[b] (b ascending); out[L*L] = sum of all weight
@@ -84,7 +92,8 @@ int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaS
   const int one = 1;
   cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, stream);
   if (count) {
-    finite_kernel<<<1184, 256, 0, stream>>>(data, count, dflag);
+    const size_t blocks = std::min<size_t>(148 * 8, (count / 4 + 255) / 256 + 1);
+    finite_kernel<<<unsigned(blocks), 256, 0, stream>>>(data, count, dflag);
     mrf::note_launch();
   }
   int h = 0;

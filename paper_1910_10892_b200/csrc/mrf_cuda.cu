@@ -206,6 +206,20 @@ void validate_problem(mrf_topology_t topo, const mrf_problem_f32* pr) {
   if (!pr->weight_planes && !(pr->weight >= 0.0f)) fail(MRF_EINVAL, "edge weight must be nonnegative");
 }
 
+}  // namespace
+extern "C" int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaStream_t stream);
+namespace {
+
+// The reference engines reject non-finite unaries (isgmr.hpp:32-35,
+// trwp.hpp:33-36); one scan per forward call unless the caller opts out.
+void require_finite(const mrf_problem_f32* pr, int N, const char* who, cudaStream_t stream) {
+  if (pr->assume_finite) return;
+  int ok = 0;
+  const int rc = mrf_check_finite_f32(pr->unary, size_t(pr->batch) * N * pr->labels, &ok, stream);
+  if (rc != MRF_OK) fail(rc, std::string(who) + ": finiteness scan failed");
+  if (!ok) fail(MRF_EINVAL, std::string(who) + ": non-finite unary potential");
+}
+
 void validate_rho(const mrf_problem_f32* pr) {
   if (!pr->rho_planes && !(pr->rho > 0.0f && pr->rho <= 1.0f)) fail(MRF_EINVAL, "rho must be in (0, 1]");
 }
@@ -268,10 +282,12 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
   // The pairwise strategy is only known on the device (desc), so the banded
   // D == 2 specialisation and the generic kernel are both launched; each
   // returns at once when the other one owns the sweep.
-  const bool band2 = g.R == 4 || g.R == 8;
-  const bool small = fwd_small_applies(g.L, g.R);
+  // Diagnostic mode (pr->diag_gap): only the generic kernel, dense, tracking gaps.
+  const bool diag = pr->diag_gap != nullptr;
+  const bool band2 = !diag && (g.R == 4 || g.R == 8);
+  const bool small = !diag && fwd_small_applies(g.L, g.R);
   FwdArgs a{g, make_potentials(pr), lines, nlines, m_in, m_out, p, q, k, desc, band2 ? 1 : 0, band2 ? fwd_bandw_max() : 0,
-            small ? 1 : 0, agg_cost, agg_labels, dir};
+            small ? 1 : 0, agg_cost, agg_labels, dir, pr->diag_gap};
   ProfScope ps(stream, MRF_KCLASS_FWD_SWEEP);
   if (band2) {
     cuda_check(TRWP ? launch_fwd_band2_trwp(a, pr->batch, stream) : launch_fwd_band2_isgmr(a, pr->batch, stream),
@@ -335,6 +351,9 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
   if (int64_t(R) * N * L >= (int64_t(1) << 31) || int64_t(K) * topo->host.total_edges() * L >= (int64_t(1) << 32))
     fail(MRF_EINVAL, "backward: image too large (R*N*L must be < 2^31 and K*E*L < 2^32)");
+  // edge indices over the whole batch are 32-bit in the backward kernels
+  if (int64_t(B) * K * topo->host.total_edges() >= (int64_t(1) << 32))
+    fail(MRF_EINVAL, "backward: batch too large for one call (B*K*E must be < 2^32)");
   char* w = static_cast<char*>(ws);
   float* A[2] = {reinterpret_cast<float*>(w), TRWP ? nullptr : reinterpret_cast<float*>(w + align_up(mb))};
   float* gvacc = reinterpret_cast<float*>(w + align_up(mb) * (TRWP ? 1 : 2));
@@ -465,6 +484,7 @@ int mrf_isgmr_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
     validate_problem(topo, prob);
     if (iterations < 1) fail(MRF_EINVAL, "isgmr_forward: iterations must be >= 1");
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
+    require_finite(prob, topo->host.nodes(), "isgmr_forward", stream);
     const size_t mb = messages_bytes(topo, prob);
     if (!workspace || workspace_bytes < mb) fail(MRF_EINVAL, "forward workspace too small");
     float* bufs[2] = {out->messages, static_cast<float*>(workspace)};
@@ -491,11 +511,15 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
     validate_rho(prob);
     if (iterations < 1) fail(MRF_EINVAL, "trwp_forward: iterations must be >= 1");
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
+    require_finite(prob, topo->host.nodes(), "trwp_forward", stream);
     cuda_check(cudaMemsetAsync(out->messages, 0, messages_bytes(topo, prob), stream), "zero m");
     PairDescHolder desc(prob, topo->host.num_dirs(), stream);
     // 4 directions: the last sweep's banded D == 2 kernel aggregates on the
-    // fly (every node is a prev or the tail of one of its lines)
-    const bool fuse = topo->host.num_dirs() == 4 && (out->cost || out->labels);
+    // fly (every node is a prev or the tail of one of its lines). Direction 3
+    // runs along columns, so this needs H >= 2: with H == 1 it has no line of
+    // two nodes and never launches.
+    const bool fuse = topo->host.num_dirs() == 4 && topo->host.height() >= 2 && !prob->diag_gap &&
+                      (out->cost || out->labels);
     for (int k = 0; k < iterations; ++k) {
       const bool last = fuse && k == iterations - 1;
       trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, desc.get(), stream,

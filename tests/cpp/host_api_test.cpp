@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <optional>
 #include <random>
 
 #include "mrf/mp_cuda.hpp"
@@ -84,7 +85,99 @@ static void run_case(bool trwp, int H, int W, int L, int conn, int K, bool plane
   orc_topo_free(ot);
 }
 
+// Engine classes (isgmr.hpp:26-68, trwp.hpp:25-68): step() K times; after
+// every step the messages, the aggregated cost/labels and the indices so far
+// equal the oracle's K=k+1 forward; take_indices() feeds the backward;
+// *_iterate_energy (isgmr.hpp:156-169, trwp.hpp:158-171) equals the energy
+// of the oracle's labelling after each iteration.
+static void engine_case(bool trwp, int H, int W, int L, int conn, int K, uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> uu(0.0, 10.0);
+  const GridTopology topo(GridGraph(H, W), DirectionSet::build(conn));
+  PotentialSet<float> pots;
+  pots.unary = UnaryVolume<float>(H, W, L);
+  for (auto& v : pots.unary.values) v = float(uu(rng));
+  pots.pairwise = build_pairwise<float>(PairwiseKind::truncated_linear, {2.0, 1.0, 1.0}, L);
+  pots.weights = EdgeWeights<float>::constant(1.25f);
+  const auto rho = default_rho<float>(conn, 0.5f);
+  orc_problem pr{H, W, L, pots.unary.values.data(), pots.pairwise.table.data(), 1.25f, nullptr, 0.5f, nullptr};
+  orc_topo* ot = orc_topo_create(H, W, conn);
+  const size_t n = size_t(H) * W, E = size_t(orc_total_edges(ot));
+  std::optional<IsgmrEngine<float>> ie;
+  std::optional<TrwpEngine<float>> te;
+  if (trwp)
+    te.emplace(topo, pots, rho, 4);
+  else
+    ie.emplace(topo, pots, 4);
+  std::vector<double> energies;
+  for (int k = 0; k < K; ++k) {
+    if (trwp)
+      te->step();
+    else
+      ie->step();
+    const int kk = k + 1;
+    std::vector<float> cost(n * L), msg(size_t(conn) * n * L);
+    std::vector<uint16_t> lab(n);
+    std::vector<uint8_t> p(kk * E * L), q(kk * E);
+    (trwp ? orc_trwp_forward : orc_isgmr_forward)(ot, &pr, kk, cost.data(), lab.data(), msg.data(), p.data(), q.data());
+    const auto agg = trwp ? te->aggregate() : ie->aggregate();
+    const auto& m = trwp ? te->messages() : ie->messages();
+    const auto& idx = trwp ? te->indices() : ie->indices();
+    CHECK((trwp ? te->iterations() : ie->iterations()) == kk);
+    CHECK(std::memcmp(m.data(), msg.data(), 4 * msg.size()) == 0);
+    CHECK(std::memcmp(agg.cost.data(), cost.data(), 4 * cost.size()) == 0);
+    CHECK(agg.labels_map == lab);
+    CHECK(idx.iterations() == kk && idx.p_data() == p && idx.q_data() == q);
+    CHECK(std::isinf(trwp ? te->min_argmin_gap() : ie->min_argmin_gap()));  // not tracked outside diagnostic mode
+    energies.push_back(energy(topo, pots, lab));
+  }
+  IndexStore st = trwp ? te->take_indices() : ie->take_indices();
+  CHECK(st.iterations() == K && st.bytes() == K * E * (L + 1));
+  std::vector<float> gc(n * L, 1.0f / float(n * L));
+  const auto g = trwp ? trwp_backward(topo, pots, rho, st, gc) : isgmr_backward(topo, pots, st, gc);
+  std::vector<float> gu(n * L), gv(size_t(L) * L), gw((conn / 2) * n);
+  (trwp ? orc_trwp_backward : orc_isgmr_backward)(ot, &pr, K, st.p_data().data(), st.q_data().data(), gc.data(),
+                                                  gu.data(), gv.data(), gw.data());
+  CHECK(normwise(g.unary, gu) < 1e-5);
+  CHECK(normwise(g.pairwise, gv) < 1e-5);
+  const auto it = trwp ? trwp_iterate_energy(topo, pots, rho, K) : isgmr_iterate_energy(topo, pots, K);
+  CHECK(it.size() == energies.size());
+  for (size_t k = 0; k < it.size() && k < energies.size(); ++k)
+    CHECK(std::fabs(it[k] - energies[k]) <= 1e-9 * std::fabs(energies[k]));
+  // diagnostic mode: same messages, a finite gap
+  if (trwp) {
+    TrwpEngine<float> d(topo, pots, rho, 1, true);
+    for (int k = 0; k < K; ++k) d.step();
+    CHECK(d.messages() == te->messages());
+    CHECK(std::isfinite(d.min_argmin_gap()) && d.min_argmin_gap() >= 0.f);
+  } else {
+    IsgmrEngine<float> d(topo, pots, 1, true);
+    for (int k = 0; k < K; ++k) d.step();
+    CHECK(d.messages() == ie->messages());
+    CHECK(std::isfinite(d.min_argmin_gap()) && d.min_argmin_gap() >= 0.f);
+  }
+  orc_topo_free(ot);
+}
+
 int main() {
+  engine_case(false, 8, 11, 24, 4, 5, 11);  // 5 steps: the device index store regrows past capacity
+  engine_case(true, 9, 7, 40, 4, 3, 12);
+  engine_case(true, 6, 10, 7, 8, 4, 13);
+  {
+    // the engines reject non-finite unaries like the reference constructors
+    PotentialSet<float> bad;
+    bad.unary = UnaryVolume<float>(3, 3, 2);
+    bad.unary.values[5] = std::nanf("");
+    bad.pairwise = build_pairwise<float>(PairwiseKind::potts, {}, 2);
+    const GridTopology t3(GridGraph(3, 3), DirectionSet::build(4));
+    bool threw = false;
+    try {
+      TrwpEngine<float> e(t3, bad, default_rho<float>(4, 0.5f));
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   run_case(false, 7, 9, 5, 4, 3, true, 1);
   run_case(true, 7, 9, 5, 8, 3, true, 2);
   run_case(false, 9, 6, 16, 8, 2, false, 3);

@@ -50,6 +50,8 @@ CASES = [
     (9, 14, 21, 8, 2, True, True),
     (3, 17, 1, 4, 3, False, True),
     (1, 12, 5, 4, 1, False, True),
+    (1, 12, 16, 4, 2, False, False),  # banded TRWP-4 on one row: no vertical line to fuse into
+    (2, 9, 24, 4, 2, False, False),
     (12, 1, 7, 8, 2, True, False),
     (10, 12, 32, 4, 2, False, True),
     (8, 9, 33, 4, 2, True, True),
@@ -125,8 +127,14 @@ def test_c5_shaped_integer_ties():
 
 
 @pytest.mark.parametrize("engine", ["isgmr", "trwp"])
-def test_batch_images_independent(engine):
-    H, W, L, conn, K, B = 11, 9, 21, 4, 2, 3
+@pytest.mark.parametrize("shape", [(11, 9, 21, 4, 2, 3), (7, 10, 21, 4, 3, 2), (7, 10, 5, 8, 3, 3),
+                                   (7, 10, 192, 4, 3, 2), (5, 8, 30, 4, 1, 3)],
+                         ids=["11x9L21K2", "7x10L21K3", "7x10L5c8K3", "7x10L192K3", "5x8L30K1"])
+def test_batch_images_independent(engine, shape):
+    """Images of a batch are independent. The odd-K / odd-(H+W) shapes put
+    image b >= 1's p and q rows at byte offsets that are not word aligned
+    (K*E % 4 != 0, K*E*L % 4 != 0)."""
+    H, W, L, conn, K, B = shape
     uns, pls, rhos, refs = [], [], [], []
     V = None
     for b in range(B):
@@ -257,3 +265,69 @@ def test_band2_ring_depths_bit_exact(case, engine, stages, monkeypatch):
     pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
     ref = O.forward(engine, pr, K)
     assert_forward_equal(gpu_forward(engine, to_mrf(pr), K), ref)
+
+
+GAP_CASES = [(7, 9, 5, 4, 3, True, True), (6, 8, 40, 8, 2, False, False), (5, 6, 192, 4, 2, False, False),
+             (9, 7, 21, 4, 2, True, True), (4, 5, 256, 8, 1, False, True), (1, 9, 3, 4, 2, False, True)]
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", GAP_CASES, ids=[f"{c[0]}x{c[1]}L{c[2]}c{c[3]}" for c in GAP_CASES])
+def test_diagnostic_min_argmin_gap_matches_reference(engine, case):
+    """Diagnostic mode (mrf_problem_f32::diag_gap): min_argmin_gap equals the
+    reference's ForwardResult::min_argmin_gap (isgmr.hpp:64-68,109-129,
+    trwp.hpp:57-59), and messages / indices stay bit-identical."""
+    if not O.have_ref():
+        pytest.skip("reference library not present")
+    H, W, L, conn, K, per_edge, explicit = case
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=H * 31 + L, per_edge=per_edge, explicit=explicit)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K, impl="ref", threads=1)
+    mrf = to_mrf(pr)
+    f = (api.isgmr_forward if engine == "isgmr" else api.trwp_forward)(mrf, K, diagnostic=True)
+    torch.cuda.synchronize()
+    assert_forward_equal(f, ref)
+    assert f.min_argmin_gap[0].item() == ref.gap
+    eng = (api.IsgmrEngine if engine == "isgmr" else api.TrwpEngine)(mrf, 1, diagnostic=True)
+    for _ in range(K):
+        eng.step()
+    assert eng.min_argmin_gap()[0].item() == ref.gap
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+def test_engine_index_store_grows(engine):
+    """step() past the initial capacity regrows the device index store (the
+    reference's append_iteration); indices of every iteration survive."""
+    H, W, L, conn, K = 6, 7, 16, 4, 5
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=8, explicit=False)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    eng = (api.IsgmrEngine if engine == "isgmr" else api.TrwpEngine)(to_mrf(pr), 1)
+    for _ in range(K):
+        eng.step()
+    p, q = eng.indices()
+    assert eng.iterations() == K
+    assert np.array_equal(p[0].cpu().numpy().reshape(-1), ref.p)
+    assert np.array_equal(q[0].cpu().numpy().reshape(-1), ref.q)
+    assert np.array_equal(bits_(eng.messages()[0]), bits_(ref.messages))
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+def test_non_finite_unary_rejected_at_the_c_abi(engine):
+    """The forward entry points reject NaN / Inf unaries with MRF_EINVAL (the
+    reference engines throw std::invalid_argument, isgmr.hpp:32-35,
+    trwp.hpp:33-36); engines reject them at construction."""
+    H, W, L, conn = 5, 6, 7, 4
+    un, V, wc, _ = WL.random_problem(H, W, L, conn, seed=3)
+    for bad in (float("nan"), float("inf"), float("-inf")):
+        x = un.copy()
+        x[17] = bad
+        mrf = to_mrf(O.Problem(H, W, L, conn, x, V, wc, None, 0.5, None))
+        fwd = api.isgmr_forward if engine == "isgmr" else api.trwp_forward
+        with pytest.raises(ValueError, match="non-finite"):
+            fwd(mrf, 2)
+        with pytest.raises(ValueError, match="non-finite"):
+            (api.IsgmrEngine if engine == "isgmr" else api.TrwpEngine)(mrf, 2)
+        mrf.assume_finite = True  # caller's promise: no scan, no error
+        fwd(mrf, 1)
+        torch.cuda.synchronize()
