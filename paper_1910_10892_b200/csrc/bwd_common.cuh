@@ -40,7 +40,17 @@
 
 namespace mrf {
 
-constexpr int kVRep = 4;  // dV accumulation replicas per image
+// dV accumulation: every CTA (bwd_split) / warp (bwd_small) owns a private
+// [L][L] slot per image, accumulated over all sweeps of the backward (lines
+// are assigned to CTAs statically) and reduced over the slots in a fixed order
+// at the end, so dV is bit-identical run to run (the reference's per-scanline
+// partials reduced in order, autodiff.hpp:119-120, test_autodiff.cpp:86-110).
+// Within a slot every addition is ordered: one warp writes it, lanes of one
+// instruction hit distinct entries and successive instructions are separated
+// by __syncwarp().
+constexpr int kDvSlotsSplit = 592;      // persistent CTAs per image of bwd_split (<= 4 per SM)
+constexpr int kDvSlotsSmall = 592 * 4;  // warps per image of bwd_small
+__host__ __device__ inline int dv_slots_for(int L) { return L <= 32 ? kDvSlotsSmall : kDvSlotsSplit; }
 
 struct AccArgs {
   Geometry g;
@@ -54,9 +64,11 @@ struct AccArgs {
   const float* ain;  // [B][R][N][L] planes read (TRWP: == aout; ISGMR: iteration k+1)
   float* aout;       // [B][R][N][L] planes written (plane r of each line)
   float* gw;         // TRWP: [B][R/2][N] (family planes); ISGMR: [B][R][N] per direction; or null
-  float* gvacc;      // [B][kVRep][2][L][L]
+  float* gvacc;      // [B][dv_slots][L][L] private dV slots, V orientation (x = first label)
+  int dv_slots;
   const PairDesc* desc;
   float* dtheta;     // TRWP direction 0: dtheta += rho_d A[d] of the iteration, fused (else null)
+  const float* dtheta_src;  // the running dtheta read by that update: dc on the first one (no dc -> dtheta copy)
 };
 
 // row slots: TRWP R-1 planes (+ dc at k == K-1: at most R), ISGMR R-2 planes or dc
@@ -75,11 +87,14 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 // == 0 (a vector never straddles two nodes).
 template <bool TRWP>
 __global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__ A, float rho,
-                                  const float* __restrict__ rho_planes, Geometry g, float* __restrict__ dtheta) {
+                                  const float* __restrict__ rho_planes, Geometry g, float* __restrict__ dtheta,
+                                  const float* dtheta_src) {
+  // dtheta = dtheta_src + sum_d rho_d A[d]; dtheta_src is dc on the first update
   const int NL = N * L;
   const int b = blockIdx.y;
   const float* Ab = A + size_t(b) * R * NL;
   float* dt = dtheta + size_t(b) * NL;
+  const float* ds = dtheta_src + size_t(b) * NL;
   auto rho_of = [&](int d, int n) {
     if (!TRWP) return 1.0f;
     if (!rho_planes) return rho;
@@ -99,7 +114,7 @@ __global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__
         }
         s.x = fadd(s.x, v.x), s.y = fadd(s.y, v.y), s.z = fadd(s.z, v.z), s.w = fadd(s.w, v.w);
       }
-      float4 o = reinterpret_cast<float4*>(dt)[i];
+      float4 o = reinterpret_cast<const float4*>(ds)[i];
       o.x = fadd(o.x, s.x), o.y = fadd(o.y, s.y), o.z = fadd(o.z, s.z), o.w = fadd(o.w, s.w);
       reinterpret_cast<float4*>(dt)[i] = o;
     }
@@ -111,7 +126,7 @@ __global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__
         const float v = __ldcs(Ab + size_t(d) * NL + i);
         s = fadd(s, TRWP ? fmul(rho_of(d, n), v) : v);
       }
-      dt[i] = fadd(dt[i], s);
+      dt[i] = fadd(ds[i], s);
     }
   }
 }
@@ -125,19 +140,25 @@ static __global__ void combine_dw_kernel(int B, int R, int N, const float* __res
   }
 }
 
-// dV[b][x][y] = sum_rep acc[b][rep][0][x][y] + acc[b][rep][1][y][x]
-static __global__ void reduce_gvacc_kernel(int B, int L, const float* __restrict__ acc, float* __restrict__ gv) {
+// dV[b][xy] = sum over slots s = 0, 1, ... of acc[b][s][xy], in slot order
+// (deterministic). Slots are summed in chunks of 8 loads in flight.
+static __global__ void reduce_gvacc_kernel(int B, int L, int slots, int used, const float* __restrict__ acc,
+                                           float* __restrict__ gv) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t LL = int64_t(L) * L;
   if (i >= B * LL) return;
-  const int b = int(i / LL);
-  const int xy = int(i - b * LL), x = xy / L, y = xy - x * L;
+  const int64_t b = i / LL, xy = i - b * LL;
+  const float* base = acc + size_t(b) * slots * LL + xy;
   float s = 0.0f;
-  for (int rep = 0; rep < kVRep; ++rep) {
-    const float* base = acc + (size_t(b) * kVRep + rep) * 2 * LL;
-    s = fadd(s, base[xy]);
-    s = fadd(s, base[LL + size_t(y) * L + x]);
+  int t = 0;
+  for (; t + 8 <= used; t += 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldcs(base + size_t(t + u) * LL);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = fadd(s, v[u]);
   }
+  for (; t < used; ++t) s = fadd(s, __ldcs(base + size_t(t) * LL));
   gv[i] = s;
 }
 

@@ -9,6 +9,18 @@
 
 namespace mrf {
 
+// Persistent grid: at most one wave of resident CTAs (and at most
+// kDvSlotsSplit, the private dV slots per image); CTA c sweeps lines c, c + G,
+// ... (lines sorted longest first), the same lines in every call.
+static int split_grid(const void* kern, int threads, int smem, int nlines) {
+  int dev = 0, sms = 148, occ = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem) != cudaSuccess || occ < 1) occ = 1;
+  const int g = occ * sms < kDvSlotsSplit ? occ * sms : kDvSlotsSplit;
+  return nlines < g ? nlines : g;
+}
+
 template <int EPL, bool TRWP, int RT, bool FULL, int MODE>
 static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   constexpr int NPRE = kSplitPre;
@@ -16,7 +28,7 @@ static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   auto kern = bwd_split_kernel<EPL, TRWP, RT, FULL, NPRE, MODE>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  const int blocks = a.nlines < 65535 ? a.nlines : 65535;
+  const int blocks = split_grid(reinterpret_cast<const void*>(kern), 32 * (2 + NPRE), smem, a.nlines);
   kern<<<dim3(blocks, batch), 32 * (2 + NPRE), smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }
@@ -47,7 +59,9 @@ static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
   auto kern = bwd_small_kernel<TRWP, RT>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
+  // at most kDvSlotsSmall warps per image (one private dV slot each)
+  const int want = (a.nlines + wpc - 1) / wpc;
+  const int blocks = want < kDvSlotsSmall / wpc ? want : kDvSlotsSmall / wpc;
   kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a); note_launch();
   return cudaGetLastError();
 }

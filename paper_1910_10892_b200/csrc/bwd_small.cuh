@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     const int nsteps = ld.length - 1;
     const int stL = st * L;
     const int o_first = ld.first * L;
-    float* gvacc = a.gvacc + ((size_t(b) * kVRep + warp_global % kVRep) * 2 + (r & 1)) * L * L;
+    // this warp's private dV slot, V orientation (bwd_common.cuh)
+    float* gvacc = a.gvacc + (size_t(b) * a.dv_slots + warp_global) * L * L;
+    const int vs_mu = (r & 1) ? 1 : L, vs_l = (r & 1) ? L : 1;
     const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     float* gwrow = do_w ? a.gw + (TRWP ? (size_t(b) * (R / 2) + fam) * N : (size_t(b) * R + r) * N) : nullptr;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     const int npl = nrows;  // plane rows end here
     const bool fuse = TRWP && a.dtheta != nullptr;
     float* dthb = fuse ? a.dtheta + size_t(b) * NL : nullptr;
+    const float* dths = fuse ? a.dtheta_src + size_t(b) * NL : nullptr;  // running dtheta (dc on the first update)
     // edge index over the whole batch: p/q words are addressed from a.p/a.q so
     // that byte offsets stay word-aligned for any b, K_cap and E (K*E odd)
     const uint32_t ebase = (uint32_t(b) * uint32_t(g.K_cap) + uint32_t(a.k)) * uint32_t(g.E) + uint32_t(g.dir_offset[r]) + uint32_t(ld.edge_base);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     if (valid) aoutb[size_t(r) * NL + o_first + nsteps * stL] = 0.0f;
     float carry = 0.0f;
     // fused unary gradient: dtheta(cur) loaded one step ahead
-    float dtn = (fuse && valid && nsteps > 0) ? __ldcg(dthb + o_first + nsteps * stL + lane) : 0.0f;
+    float dtn = (fuse && valid && nsteps > 0) ? __ldcg(dths + o_first + nsteps * stL + lane) : 0.0f;
 
     for (int s = 0; s < nsteps; ++s) {
       if (s + kStages - 1 < nsteps) issue(s + kStages - 1);
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
       // fused unary gradient: dtheta(cur) += sum_d rho_d A[d](cur) + this sweep's share
       if (fuse && valid) {
         const float dnew = fadd(fadd(dtn, rsum), carry);
-        if (s + 1 < nsteps) dtn = __ldcg(dthb + o_first + (j - 1) * stL + lane);
+        if (s + 1 < nsteps) dtn = __ldcg(dths + o_first + (j - 1) * stL + lane);
         dthb[o_first + j * stL + lane] = dnew;
       }
       carry = TRWP ? fmul(rho, acc) : acc;
@@ -264,15 +267,14 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
         }
         hs = fadd(hs, fmul(rd, __ldcg(ainb + size_t(d) * NL + size_t(head) * L)));
       }
-      float* dst = dthb + size_t(head) * L + lane;
-      *dst = fadd(fadd(*dst, hs), carry);
+      dthb[size_t(head) * L + lane] = fadd(fadd(dths[size_t(head) * L + lane], hs), carry);
     }
     // flush this line's dV partials (lane l owns column l)
     if (valid) {
       for (int m = 0; m < L; ++m) {
         const float v = s_dv[m * 32 + lane];
         if (v != 0.0f) {
-          red_add_global(gvacc + m * L + lane, v);
+          red_add_global(gvacc + m * vs_mu + lane * vs_l, v);
           s_dv[m * 32 + lane] = 0.0f;
         }
       }

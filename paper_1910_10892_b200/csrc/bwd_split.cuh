@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
         // overlaps the decode (POST then only adds the carry)
         float dto[EPL];
         if (fuse) {
-          const float* src = a.dtheta + size_t(b) * NL + o_first + j * stL + l0;
+          const float* src = a.dtheta_src + size_t(b) * NL + o_first + j * stL + l0;
           if (FULL && EPL % 2 == 0) {
 #pragma unroll
             for (int i = 0; i < EPL; i += 2) {
@@ -662,7 +662,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
     } else {
       // =============================== POST ==============================
       float* aout_r = a.aout + size_t(b) * R * NL + size_t(r) * NL;
-      float* gvacc = a.gvacc + ((size_t(b) * kVRep + blockIdx.x % kVRep) * 2 + (r & 1)) * L * L;
+      // this CTA's private dV slot; entry (mu, l) of V' is V[mu][l] (even r) / V[l][mu] (odd r)
+      float* gvacc = a.gvacc + (size_t(b) * a.dv_slots + blockIdx.x) * L * L;
       const int vs_mu = (r & 1) ? 1 : L, vs_l = (r & 1) ? L : 1;
       float* gwrow = do_w ? a.gw + (TRWP ? (size_t(b) * (R / 2) + fam) * N : (size_t(b) * R + r) * N) : nullptr;
       const float* gband = a.desc->g;
@@ -686,7 +687,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
       auto flush_far = [&]() {
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
-          if (fval[i] != 0.0f) red_add_global(gvacc + fkey * L + l0 + i, fmul(fval[i], wfold));
+          if (fval[i] != 0.0f) red_add_global(gvacc + fkey * vs_mu + (l0 + i) * vs_l, fmul(fval[i], wfold));
           fval[i] = 0.0f;
         }
       };
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
             float gv = fadd(sl[SL::X + src], sl[SL::CIN + src]);
             if (src == qv) gv = fsub(gv, S);
             const float gwv = fmul(gv, w);
-            if (gwv != 0.0f) red_add_global(gvacc + tgt * L + src, gwv);
+            if (gwv != 0.0f) red_add_global(gvacc + tgt * vs_mu + src * vs_l, gwv);
           }
         }
         __syncwarp();
@@ -826,8 +827,8 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
 #pragma unroll
         for (int i = 0; i < EPL; ++i) {
           if (FULL || i < nvalid) {
-            float* dst = dthb + size_t(head) * L + l0 + i;
-            *dst = fadd(fadd(*dst, hs[i]), nsteps > 0 ? fmul(rhol, accl[i]) : 0.0f);
+            const size_t o = size_t(b) * NL + size_t(head) * L + l0 + i;
+            a.dtheta[o] = fadd(fadd(a.dtheta_src[o], hs[i]), nsteps > 0 ? fmul(rhol, accl[i]) : 0.0f);
           }
         }
       }
@@ -838,7 +839,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
           const float v = s_dv[t];
           if (v != 0.0f) {
             const int l = t / (2 * kWin + 1), m = l + t % (2 * kWin + 1) - kWin;
-            red_add_global(gvacc + m * L + l, fmul(v, wfold));
+            red_add_global(gvacc + m * vs_mu + l * vs_l, fmul(v, wfold));
             s_dv[t] = 0.0f;
           }
         }
@@ -850,7 +851,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a
 #pragma unroll
           for (int t = 0; t < 3; ++t) {
             const int m = l + t - 1;
-            if (l < L && m >= 0 && m < L && vacc[i][t] != 0.0f) red_add_global(gvacc + m * L + l, fmul(vacc[i][t], wfold));
+            if (l < L && m >= 0 && m < L && vacc[i][t] != 0.0f) red_add_global(gvacc + m * vs_mu + l * vs_l, fmul(vacc[i][t], wfold));
           }
         }
       }

@@ -14,6 +14,8 @@ namespace mrf {
 
 // every kernel launch of the library is counted (mrf_launch_count)
 void note_launch();
+// clears *flag when data[0:count) holds Inf / NaN (misc.cu)
+cudaError_t launch_finite_scan(const float* data, size_t count, int* flag, cudaStream_t stream);
 
 // labels per lane for the warp-per-scanline kernels
 inline int epl_for(int L) {

@@ -57,30 +57,55 @@ __global__ void finite_kernel(const float* __restrict__ x, size_t n, int* flag) 
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 0;
 }
 
-// out[0:L*L] = sum_b pairwise[b] (b ascending); out[L*L] = sum of all weight
-// planes (GradientSet::edge_weight_total, autodiff.hpp:24-28), one block.
-__global__ void pack_kernel(int B, int L, int64_t plane_elems, const float* __restrict__ gv, const float* __restrict__ gw,
+// Shared-gradient pack, deterministic (fixed partition, fixed-order sums):
+// pack_dw_kernel: block j sums the contiguous chunk j of all weight-plane
+// gradients (grid-size independent of the device) into part[j];
+// pack_kernel: out[0:L*L] = sum_b pairwise[b] (b ascending) and out[L*L] =
+// sum_j part[j] (GradientSet::edge_weight_total, autodiff.hpp:24-28).
+constexpr int kPackChunks = 1024;
+
+__global__ void __launch_bounds__(256) pack_dw_kernel(int64_t n, const float* __restrict__ gw, float* __restrict__ part) {
+  const int64_t per = (n + kPackChunks - 1) / kPackChunks;
+  const int64_t lo = int64_t(blockIdx.x) * per, hi = lo + per < n ? lo + per : n;
+  float s = 0.0f;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s = mrf::fadd(s, gw[i]);
+  __shared__ float red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (int(threadIdx.x) < o) red[threadIdx.x] = mrf::fadd(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void pack_kernel(int B, int L, const float* __restrict__ gv, const float* __restrict__ part,
                             float* __restrict__ out) {
   const int LL = L * L;
-  for (int i = threadIdx.x; i < LL; i += blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < LL; i += gridDim.x * blockDim.x) {
     float s = 0.0f;
     for (int b = 0; b < B; ++b) s = mrf::fadd(s, gv[size_t(b) * LL + i]);
     out[i] = s;
   }
-  __shared__ float part[1024];
-  float s = 0.0f;
-  if (gw)
-    for (int64_t i = threadIdx.x; i < int64_t(B) * plane_elems; i += blockDim.x) s = mrf::fadd(s, gw[i]);
-  part[threadIdx.x] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     float t = 0.0f;
-    for (int i = 0; i < int(blockDim.x); ++i) t = mrf::fadd(t, part[i]);
+    if (part)
+      for (int j = 0; j < kPackChunks; ++j) t = mrf::fadd(t, part[j]);
     out[LL] = t;
   }
 }
 
 }  // namespace
+
+namespace mrf {
+cudaError_t launch_finite_scan(const float* data, size_t count, int* flag, cudaStream_t stream) {
+  if (!count) return cudaSuccess;
+  const size_t blocks = std::min<size_t>(148 * 8, (count / 4 + 255) / 256 + 1);
+  finite_kernel<<<unsigned(blocks), 256, 0, stream>>>(data, count, flag);
+  note_launch();
+  return cudaGetLastError();
+}
+}  // namespace mrf
 
 extern "C" {
 
@@ -91,11 +116,7 @@ int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaS
   if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? MRF_ENOMEM : MRF_ECUDA;
   const int one = 1;
   cudaMemcpyAsync(dflag, &one, sizeof(int), cudaMemcpyHostToDevice, stream);
-  if (count) {
-    const size_t blocks = std::min<size_t>(148 * 8, (count / 4 + 255) / 256 + 1);
-    finite_kernel<<<unsigned(blocks), 256, 0, stream>>>(data, count, dflag);
-    mrf::note_launch();
-  }
+  mrf::launch_finite_scan(data, count, dflag, stream);
   int h = 0;
   cudaMemcpyAsync(&h, dflag, sizeof(int), cudaMemcpyDeviceToHost, stream);
   cudaFreeAsync(dflag, stream);
@@ -108,10 +129,18 @@ int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaS
 int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const mrf_grads_f32* grads, float* out,
                               cudaStream_t stream) {
   if (!prob || !grads || !grads->pairwise || !out || prob->batch < 1 || prob->labels < 1) return MRF_EINVAL;
-  const int64_t plane_elems = int64_t(num_dirs / 2) * prob->height * prob->width;
-  pack_kernel<<<1, 1024, 0, stream>>>(prob->batch, prob->labels, plane_elems, grads->pairwise, grads->weight_planes,
-                                      out);
+  const int64_t n = int64_t(prob->batch) * (num_dirs / 2) * prob->height * prob->width;
+  float* part = nullptr;
+  if (grads->weight_planes) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&part), sizeof(float) * kPackChunks, stream) != cudaSuccess)
+      return MRF_ENOMEM;
+    pack_dw_kernel<<<kPackChunks, 256, 0, stream>>>(n, grads->weight_planes, part);
+    mrf::note_launch();
+  }
+  const int LL = prob->labels * prob->labels;
+  pack_kernel<<<(LL + 255) / 256, 256, 0, stream>>>(prob->batch, prob->labels, grads->pairwise, part, out);
   mrf::note_launch();
+  if (part) cudaFreeAsync(part, stream);
   return cudaGetLastError() == cudaSuccess ? MRF_OK : MRF_ECUDA;
 }
 

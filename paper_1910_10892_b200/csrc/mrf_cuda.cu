@@ -206,19 +206,57 @@ void validate_problem(mrf_topology_t topo, const mrf_problem_f32* pr) {
   if (!pr->weight_planes && !(pr->weight >= 0.0f)) fail(MRF_EINVAL, "edge weight must be nonnegative");
 }
 
-}  // namespace
-extern "C" int mrf_check_finite_f32(const float* data, size_t count, int* all_finite, cudaStream_t stream);
-namespace {
-
 // The reference engines reject non-finite unaries (isgmr.hpp:32-35,
-// trwp.hpp:33-36); one scan per forward call unless the caller opts out.
-void require_finite(const mrf_problem_f32* pr, int N, const char* who, cudaStream_t stream) {
-  if (pr->assume_finite) return;
-  int ok = 0;
-  const int rc = mrf_check_finite_f32(pr->unary, size_t(pr->batch) * N * pr->labels, &ok, stream);
-  if (rc != MRF_OK) fail(rc, std::string(who) + ": finiteness scan failed");
-  if (!ok) fail(MRF_EINVAL, std::string(who) + ": non-finite unary potential");
-}
+// trwp.hpp:33-36). The scan is enqueued ahead of the sweeps and writes its
+// verdict straight into mapped pinned host memory (no copy-engine operation:
+// a 4-byte copy would queue behind the caller's bulk H2D / D2H copies on the
+// copy engines and stall the compute stream); the host waits for it only
+// after it has enqueued the whole forward, so the GPU never idles on the
+// check. On MRF_EINVAL the outputs are unspecified (the reference produces
+// none).
+class FiniteCheck {
+ public:
+  FiniteCheck(const mrf_problem_f32* pr, int N, cudaStream_t s) {
+    if (pr->assume_finite) return;
+    State& st = state();
+    *st.host = 1;  // no scan of this thread is in flight (every call waits for its own)
+    cuda_check(launch_finite_scan(pr->unary, size_t(pr->batch) * N * pr->labels, st.dev, s), "finite scan");
+    cuda_check(cudaEventRecord(st.done, s), "finite event");
+    armed_ = true;
+  }
+  ~FiniteCheck() {  // an error path left the scan in flight: let it land before the flag is reused
+    if (armed_) cudaEventSynchronize(state().done);
+  }
+  FiniteCheck(const FiniteCheck&) = delete;
+  FiniteCheck& operator=(const FiniteCheck&) = delete;
+  void finish(const char* who) {
+    if (!armed_) return;
+    armed_ = false;
+    State& st = state();
+    cuda_check(cudaEventSynchronize(st.done), "finite event");
+    if (!*reinterpret_cast<volatile int*>(st.host)) fail(MRF_EINVAL, std::string(who) + ": non-finite unary potential");
+  }
+
+ private:
+  struct State {  // per host thread and device: mapped pinned verdict and an event
+    int* host = nullptr;
+    int* dev = nullptr;  // device alias of host
+    cudaEvent_t done = nullptr;
+  };
+  static State& state() {
+    thread_local std::map<int, State> states;
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    State& st = states[d];
+    if (!st.host) {
+      cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&st.host), sizeof(int), cudaHostAllocMapped), "cudaHostAlloc");
+      cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&st.dev), st.host, 0), "cudaHostGetDevicePointer");
+      cuda_check(cudaEventCreateWithFlags(&st.done, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    return st;
+  }
+  bool armed_ = false;
+};
 
 void validate_rho(const mrf_problem_f32* pr) {
   if (!pr->rho_planes && !(pr->rho > 0.0f && pr->rho <= 1.0f)) fail(MRF_EINVAL, "rho must be in (0, 1]");
@@ -330,7 +368,7 @@ void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap,
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t gvacc_bytes(const mrf_problem_f32* pr) {
-  return sizeof(float) * size_t(pr->batch) * kVRep * 2 * pr->labels * pr->labels;
+  return sizeof(float) * size_t(pr->batch) * dv_slots_for(pr->labels) * pr->labels * pr->labels;
 }
 
 size_t dwr_bytes(const mrf_problem_f32* pr, int R, int N) { return sizeof(float) * size_t(pr->batch) * R * N; }
@@ -365,8 +403,10 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
     cuda_check(cudaMemsetAsync(grads->weight_planes, 0, sizeof(float) * B * (R / 2) * N, stream), "zero dw");
   if (isgmr_dw) cuda_check(cudaMemsetAsync(dwr, 0, dwr_bytes(pr, R, N), stream), "zero dw partials");
   cuda_check(cudaMemsetAsync(gvacc, 0, vb, stream), "zero dV accumulators");
-  cuda_check(cudaMemcpyAsync(grads->unary, grad_cost, sizeof(float) * B * NL, cudaMemcpyDeviceToDevice, stream),
-             "copy grad_cost");
+  // dtheta <- dc is not copied: the first unary-gradient update reads dc
+  // directly (a device-to-device copy would also queue on a copy engine
+  // behind the caller's host transfers)
+  const float* dt_src = grad_cost;
 
   const Geometry g = make_geometry(topo, pr, K);
   const Potentials pot = make_potentials(pr);
@@ -383,25 +423,31 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       const bool fuse = !bwd_uses_small(L, int(topo->dir_lines_all[0].size()), B);
       for (int r = R - 1; r >= 0; --r) {  // directions in reverse (autodiff.hpp:147)
         AccArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), p, q, k, grad_cost,
-                  ain, aout, grads->weight_planes, gvacc, desc.get(), (r == 0 && fuse) ? grads->unary : nullptr};
+                  ain, aout, grads->weight_planes, gvacc, dv_slots_for(L), desc.get(),
+                  (r == 0 && fuse) ? grads->unary : nullptr, dt_src};
         ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         cuda_check(launch_bwd_trwp(a, B, stream), "bwd_split_kernel launch");
+        if (r == 0 && fuse) dt_src = grads->unary;
       }
       if (!fuse) {
         ProfScope ps(stream, MRF_KCLASS_AUX);
-        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary); note_launch();
+        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary,
+                                                             dt_src); note_launch();
+        dt_src = grads->unary;
         cuda_check(cudaGetLastError(), "dtheta_acc launch");
       }
     } else {
       {
         AccArgs a{g, pot, lines + topo->every_start, int(topo->every_line.size()), p, q, k, grad_cost,
-                  ain, aout, isgmr_dw ? dwr : nullptr, gvacc, desc.get(), nullptr};
+                  ain, aout, isgmr_dw ? dwr : nullptr, gvacc, dv_slots_for(L), desc.get(), nullptr, nullptr};
         ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         cuda_check(launch_bwd_isgmr(a, B, stream), "bwd_split_kernel launch");
       }
       // ISGMR's directions run concurrently: the unary gradient is collected after the launch
       ProfScope ps(stream, MRF_KCLASS_AUX);
-      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary); note_launch();
+      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary, dt_src);
+      note_launch();
+      dt_src = grads->unary;
       cuda_check(cudaGetLastError(), "dtheta_acc launch");
     }
   }
@@ -414,7 +460,8 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
     ProfScope ps(stream, MRF_KCLASS_AUX);
-    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, gvacc, grads->pairwise); note_launch();
+    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, dv_slots_for(L), dv_slots_for(L),
+                                                                           gvacc, grads->pairwise); note_launch();
     cuda_check(cudaGetLastError(), "reduce_gvacc launch");
   }
 }
@@ -484,7 +531,7 @@ int mrf_isgmr_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
     validate_problem(topo, prob);
     if (iterations < 1) fail(MRF_EINVAL, "isgmr_forward: iterations must be >= 1");
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
-    require_finite(prob, topo->host.nodes(), "isgmr_forward", stream);
+    FiniteCheck finite(prob, topo->host.nodes(), stream);
     const size_t mb = messages_bytes(topo, prob);
     if (!workspace || workspace_bytes < mb) fail(MRF_EINVAL, "forward workspace too small");
     float* bufs[2] = {out->messages, static_cast<float*>(workspace)};
@@ -499,6 +546,7 @@ int mrf_isgmr_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int 
       isgmr_step(topo, prob, k, iterations, src, dst, out->p, out->q, desc.get(), stream);
     }
     launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream);
+    finite.finish("isgmr_forward");
   });
 }
 
@@ -511,7 +559,7 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
     validate_rho(prob);
     if (iterations < 1) fail(MRF_EINVAL, "trwp_forward: iterations must be >= 1");
     if (!out || !out->messages || !out->p || !out->q) fail(MRF_EINVAL, "null forward output");
-    require_finite(prob, topo->host.nodes(), "trwp_forward", stream);
+    FiniteCheck finite(prob, topo->host.nodes(), stream);
     cuda_check(cudaMemsetAsync(out->messages, 0, messages_bytes(topo, prob), stream), "zero m");
     PairDescHolder desc(prob, topo->host.num_dirs(), stream);
     // 4 directions: the last sweep's banded D == 2 kernel aggregates on the
@@ -527,6 +575,7 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
     }
     launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream,
                      desc.get(), fuse);
+    finite.finish("trwp_forward");
   });
 }
 

@@ -1,11 +1,13 @@
 """Summarise ncu reports for profiles/.
 
-    python tools/ncu_summary.py full  <report.ncu-rep> <out.json> [label]
+    python tools/ncu_summary.py full  <report.ncu-rep> <out.json> [label] [edges] [longest_line_steps]
     python tools/ncu_summary.py launches <launches.csv> <out.json>
 
 `full`: per profiled launch -- duration, SM cycles, instructions, DRAM bytes
 read/written, registers, grid, L2 hit rate and the warp-stall breakdown
-(from `ncu --set full`). `launches`: the per-launch device-time list of
+(from `ncu --set full`), the pipe-utilisation / issue-slot counters, and --
+given the launch's edge count and longest line -- warp instructions per edge
+and ns per dependent node step. `launches`: the per-launch device-time list of
 `ncu --metrics gpu__time_duration.sum --clock-control none --csv`, grouped by
 kernel with each kernel's share of the total.
 """
@@ -17,7 +19,7 @@ import subprocess
 import sys
 
 
-def full(rep, out, label=""):
+def full(rep, out, label="", edges=0, chain_steps=0):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
@@ -41,6 +43,17 @@ def full(rep, out, label=""):
                 v = num(k)
                 if v:
                     stalls[k.replace("smsp__pcsamp_warps_issue_stalled_", "")] = v
+        # pipe utilisation and issue-slot counters (north_star: the FP32
+        # ALU / FMNMX pipe as the forward's roofline, evidenced by ncu)
+        pipes = {}
+        for k in hdr:
+            if (("pipe_" in k and (k.endswith("pct_of_peak_sustained_active") or k.endswith(".sum")))
+                    or "issue_active" in k or k.startswith("smsp__inst_executed_pipe_")
+                    or k in ("smsp__inst_executed.avg.per_cycle_active", "sm__inst_executed.avg.per_cycle_active",
+                             "sm__instruction_throughput.avg.pct_of_peak_sustained_active")):
+                v = num(k)
+                if v is not None:
+                    pipes[k] = v
         res.append({
             "kernel": d.get("Kernel Name"),
             "duration_ms": num("gpu__time_duration.sum"),
@@ -56,7 +69,17 @@ def full(rep, out, label=""):
             "block": num("launch__block_size"),
             "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "stall_samples": dict(sorted(stalls.items(), key=lambda kv: -kv[1])),
+            "pipes": pipes,
         })
+        if edges:  # per node step: work model of the scanline kernels
+            r = res[-1]
+            r["edges"] = edges
+            if r["instructions"]:
+                r["warp_instructions_per_edge"] = r["instructions"] / edges
+            if chain_steps and r["duration_ms"]:
+                # one node step of the longest line is the dependent chain of a lone warp
+                r["longest_line_steps"] = chain_steps
+                r["ns_per_chain_step"] = r["duration_ms"] * 1e6 / chain_steps
     with open(out, "w") as f:
         json.dump({"label": label, "report": rep, "launches": res}, f, indent=1)
 
@@ -82,6 +105,7 @@ def launches(path, out):
 
 if __name__ == "__main__":
     if sys.argv[1] == "full":
-        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "")
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "",
+             int(sys.argv[5]) if len(sys.argv) > 5 else 0, int(sys.argv[6]) if len(sys.argv) > 6 else 0)
     else:
         launches(sys.argv[2], sys.argv[3])
