@@ -108,15 +108,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ workloads
 
-def make_workload(cfg: str, rank: int):
-    from paper_1910_10892_b200 import workloads as WL
+GLOBAL_BATCH = {"C4": 32}  # configs whose batch is fixed and sharded over the ranks (strong scaling)
 
-    wl = WL.config(cfg)
-    if rank and wl.name in ("C1", "C2", "C3"):
-        # a different image per rank (weak scaling over independent images)
-        seed = {"C1": 1, "C2": 2, "C3": 3}[wl.name] + 1000 * rank
-        wl.unary = WL.stereo_like(wl.H, wl.W, wl.L, seed)[None]
-    return wl
+
+def make_workload(cfg: str, rank: int, world: int = 1, engine: str | None = None):
+    """This rank's workload: C4's 32-image batch is split into contiguous
+    shards (dist.shard_range; strong scaling); every other
+    config runs one image per rank, a different seeded image on each rank
+    (weak scaling over independent images)."""
+    from paper_1910_10892_b200 import workloads as WL
+    from paper_1910_10892_b200.dist import shard_range
+
+    cfg = cfg.upper()
+    if cfg in GLOBAL_BATCH:
+        start, stop = shard_range(GLOBAL_BATCH[cfg], rank, world)
+        return WL.config(cfg, batch=stop - start, first=start)
+    return WL.config(cfg, engine=engine, seed_offset=1000 * rank)
 
 
 def algorithmic_units(wl, E, E_r):
@@ -242,11 +249,11 @@ def metric_name(wl):
             f"(ms/image alongside)")
 
 
-def config_dict(wl, n):
+def config_dict(wl, n, global_batch=None):
     return {"workload": f"{wl.name}: {wl.engine.upper()} fwd+bwd, {wl.conn} directions, K={wl.K}, "
                         f"{wl.W}x{wl.H} synthetic volume, {wl.L} labels",
             "H": wl.H, "W": wl.W, "L": wl.L, "K": wl.K, "connectivity": wl.conn, "engine": wl.engine,
-            "images_per_gpu": wl.B, "global_batch": wl.B * n, "parallelism": f"dp{n}",
+            "images_per_gpu": wl.B, "global_batch": global_batch or wl.B * n, "parallelism": f"dp{n}",
             "l2": "inputs larger than L2 (unary, messages and indices each exceed 126 MB per image)"}
 
 
@@ -257,6 +264,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--engine", default=None, choices=[None, "isgmr", "trwp"], help="C5's engine (default ISGMR)")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -268,13 +276,14 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            run_reference_arm(args, make_workload(args.config, 0))
+            run_reference_arm(args, make_workload(args.config, 0, 1, args.engine))
         return
 
     import torch
     import torch.distributed as dist
 
     from paper_1910_10892_b200 import _lib, api
+    from paper_1910_10892_b200.dist import DataParallelStep, NcclComm
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -282,7 +291,8 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     _lib.lib()  # fail loudly if the CUDA library is missing
 
-    wl = make_workload(args.config, rank)
+    wl = make_workload(args.config, rank, world, args.engine)
+    global_batch = GLOBAL_BATCH.get(wl.name, world)  # images per step over all ranks
     topo = api.GridTopology(wl.H, wl.W, wl.conn)
     E = topo.total_edges
     E_r = [int(x) for x in topo.edge_count]
@@ -294,20 +304,15 @@ def main():
         w = torch.from_numpy(wl.w_planes.reshape(B, wl.conn // 2, wl.N)).to(dev)
     mrf = api.MRF(topo, unary, V, w, wl.rho_const)
     gc = torch.full_like(unary, 1.0 / (wl.N * wl.L))
-    fwd_fn = api.isgmr_forward if wl.engine == "isgmr" else api.trwp_forward
-    bwd_fn = api.isgmr_backward if wl.engine == "isgmr" else api.trwp_backward
-    fwd_out = api._alloc_forward(mrf, wl.K)
-    grads = api.GradientSet(torch.empty_like(unary), torch.empty((B, wl.L, wl.L), device=dev),
-                            torch.empty((B, wl.conn // 2, wl.N), device=dev))
-    shared = torch.empty(wl.L * wl.L + 1, device=dev)
+    # one all-reduce of the packed shared gradient per step, through the
+    # library's NCCL collective (mrf_allreduce_grads_f32)
+    comm = NcclComm(dev) if world > 1 else None
+    dp = DataParallelStep(mrf, wl.engine, wl.K, comm=comm)
+    fwd_out, grads, shared = dp.fwd, dp.grads, dp.shared
     stream = torch.cuda.current_stream()
 
     def step():
-        f = fwd_fn(mrf, wl.K, out=fwd_out)
-        bwd_fn(mrf, f, gc, out=grads)
-        api.pack_shared_grads(mrf, grads, out=shared)
-        if world > 1:
-            dist.all_reduce(shared)
+        dp.step(gc)
 
     def barrier():
         if world > 1:
@@ -358,7 +363,7 @@ def main():
         ms = float(t.item())
 
     LU, cand, fwd_bytes, bwd_bytes = algorithmic_units(wl, E, E_r)
-    images = B * world * args.steps
+    images = global_batch * args.steps
     value = LU * images / (ms / 1e3) / 1e9
     ms_per_step = ms / args.steps
 
@@ -408,14 +413,15 @@ def main():
                 "backward bytes with R+1 row read-modify-writes per node; NOT kernel efficiency"}
 
     # ---- end to end through the C-ABI with pinned host buffers
-    e2e = run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, LU, barrier)
+    e2e = run_e2e(args, wl, mrf, dp, world, global_batch, dev, LU, barrier)
 
     line = {
         "metric": metric_name(wl), "value": value, "unit": "G label-updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "ms_per_image": ms / images * world, "higher_is_better": True, "scaling": "weak",
+        "ms_per_image": ms / images * world, "higher_is_better": True,
+        "scaling": "strong" if wl.name in GLOBAL_BATCH else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded stereo-like cost volume; no datasets)",
-        "config": config_dict(wl, world), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+        "config": config_dict(wl, world, global_batch), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -424,11 +430,13 @@ def main():
                                 "sample": desc, "seconds": dt}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, LU, barrier):
+def run_e2e(args, wl, mrf, dp, world, global_batch, dev, LU, barrier):
     """Same step through the C-ABI with host buffers: every step copies its
     inputs (unary, cost gradient) from pinned host memory and reads its
     result (gradients + labels) back, all inside the timed region. Steps are
@@ -446,6 +454,7 @@ def run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, L
     d_un = [torch.empty_like(mrf.unary) for _ in range(NB)]
     d_gc = [torch.empty_like(mrf.unary) for _ in range(NB)]
     mrfs = [api.MRF(mrf.topo, d_un[i], mrf.V, mrf.weight, mrf.rho) for i in range(NB)]
+    fwd_out, grads = dp.fwd, dp.grads
     outs = [fwd_out] + [api._alloc_forward(mrf, wl.K) for _ in range(NB - 1)]
     gsets = [grads] + [api.GradientSet(torch.empty_like(grads.unary), torch.empty_like(grads.pairwise),
                                        torch.empty_like(grads.edge_weights)) for _ in range(NB - 1)]
@@ -469,11 +478,7 @@ def run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, L
         s_c.wait_event(in_done[k])
         if used[k]:
             s_c.wait_event(out_done[k])  # step i-NB's results are on the host
-        f = fwd_fn(mrfs[k], wl.K, out=outs[k])
-        bwd_fn(mrfs[k], f, d_gc[k], out=gsets[k])
-        api.pack_shared_grads(mrfs[k], gsets[k], out=shared)
-        if world > 1:
-            dist.all_reduce(shared)
+        dp.step(d_gc[k], mrf=mrfs[k], out=outs[k], grads=gsets[k])
         comp_done[k].record(s_c)
         s_out.wait_event(comp_done[k])
         with torch.cuda.stream(s_out):
@@ -505,7 +510,7 @@ def run_e2e(args, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, world, dev, L
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    images = wl.B * world * args.e2e_steps
+    images = global_batch * args.e2e_steps
     h2d = h_unary.numel() * 4 + h_gc.numel() * 4
     d2h = (hs[0]["gu"].numel() + hs[0]["gv"].numel() + hs[0]["gw"].numel()) * 4 + hs[0]["lab"].numel() * 2
     return {"value": LU * images / (ms / 1e3) / 1e9, "unit": "G label-updates/s", "h2d_bytes_per_step": h2d,

@@ -185,6 +185,15 @@ int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const m
  * per training step, over the buffer mrf_pack_shared_grads_f32 produced. */
 int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream);
 
+/* Communicator helpers for callers without their own NCCL binding (bench.py,
+ * paper_1910_10892_b200/dist.py): mrf_nccl_unique_id writes rank 0's 128-byte
+ * ncclUniqueId (broadcast it to the other ranks out of band), every rank then
+ * calls mrf_nccl_comm_init(&comm, nranks, id, rank) on its own device;
+ * mrf_nccl_comm_destroy frees it. */
+int mrf_nccl_unique_id(void* out, size_t bytes);
+int mrf_nccl_comm_init(void** comm, int nranks, const void* unique_id, int rank);
+int mrf_nccl_comm_destroy(void* comm);
+
 /* ------------------------------------------------- readout and evaluation */
 
 /* Replaces mp::soft_head_forward<float> + mp::soft_head_backward<float>

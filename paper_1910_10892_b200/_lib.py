@@ -65,6 +65,9 @@ SIGNATURES = {
     "mrf_trwp_backward_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _GR, _vp, _sz, _vp]),
     "mrf_pack_shared_grads_f32": (_i, [_PP, _i, _GR, _vp, _vp]),
     "mrf_allreduce_grads_f32": (_i, [_vp, _vp, _sz, _vp]),
+    "mrf_nccl_unique_id": (_i, [_vp, _sz]),
+    "mrf_nccl_comm_init": (_i, [C.POINTER(_vp), _i, _vp, _i]),
+    "mrf_nccl_comm_destroy": (_i, [_vp]),
     "mrf_soft_head_f32": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mrf_energy_f32": (_i, [_vp, _PP, _vp, C.POINTER(C.c_double), _vp]),
     "mrf_sgm_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _vp]),

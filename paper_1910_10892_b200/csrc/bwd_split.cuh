@@ -47,7 +47,10 @@ namespace mrf {
 
 constexpr int kSplitSlots = 4;   // node slots between the roles
 constexpr int kPreStages = 3;    // cp.async stages per PRE warp
-constexpr int kSplitPre = 3;     // PRE warps per CTA
+#ifndef MRF_SPLIT_PRE
+#define MRF_SPLIT_PRE 3
+#endif
+constexpr int kSplitPre = MRF_SPLIT_PRE;  // PRE warps per CTA (A/B: -DMRF_SPLIT_PRE=n)
 
 // ---- mbarrier helpers (CTA scope; arrive = release, try_wait = acquire)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

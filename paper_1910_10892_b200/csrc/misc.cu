@@ -6,6 +6,7 @@
 #include <atomic>
 
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
@@ -144,19 +145,74 @@ int mrf_pack_shared_grads_f32(const mrf_problem_f32* prob, int num_dirs, const m
   return cudaGetLastError() == cudaSuccess ? MRF_OK : MRF_ECUDA;
 }
 
-int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream) {
-  // ncclAllReduce(sendbuff, recvbuff, count, ncclFloat=7, ncclSum=0, comm, stream)
-  using AllReduceFn = int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t);
-  static AllReduceFn fn = nullptr;
-  if (!nccl_comm || !buffer) return MRF_EINVAL;
-  if (!fn) {
+}  // extern "C"
+
+namespace {
+
+// NCCL is resolved at run time (no link dependency): the library torch
+// already loaded when present, else the system libnccl.so.2.
+struct NcclUniqueId {
+  char internal[128];
+};
+struct Nccl {
+  int (*get_unique_id)(NcclUniqueId*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclUniqueId, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*all_reduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*get_error_string)(int) = nullptr;
+  bool ok = false;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl t;
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) return MRF_ECUDA;
-    fn = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
-    if (!fn) return MRF_ECUDA;
-  }
-  return fn(buffer, buffer, count, /*ncclFloat32*/ 7, /*ncclSum*/ 0, nccl_comm, stream) == 0 ? MRF_OK : MRF_ECUDA;
+    if (!h) return t;
+    t.get_unique_id = reinterpret_cast<decltype(t.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    t.comm_init_rank = reinterpret_cast<decltype(t.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    t.comm_destroy = reinterpret_cast<decltype(t.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    t.all_reduce = reinterpret_cast<decltype(t.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    t.get_error_string = reinterpret_cast<decltype(t.get_error_string)>(dlsym(h, "ncclGetErrorString"));
+    t.ok = t.get_unique_id && t.comm_init_rank && t.comm_destroy && t.all_reduce;
+    return t;
+  }();
+  return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrf_nccl_unique_id(void* out, size_t bytes) {
+  const Nccl& n = nccl();
+  if (!out || bytes < sizeof(NcclUniqueId)) return MRF_EINVAL;
+  if (!n.ok) return MRF_ECUDA;
+  return n.get_unique_id(static_cast<NcclUniqueId*>(out)) == 0 ? MRF_OK : MRF_ECUDA;
+}
+
+int mrf_nccl_comm_init(void** comm, int nranks, const void* unique_id, int rank) {
+  const Nccl& n = nccl();
+  if (!comm || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return MRF_EINVAL;
+  if (!n.ok) return MRF_ECUDA;
+  NcclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  return n.comm_init_rank(comm, nranks, id, rank) == 0 ? MRF_OK : MRF_ECUDA;
+}
+
+int mrf_nccl_comm_destroy(void* comm) {
+  const Nccl& n = nccl();
+  if (!comm) return MRF_EINVAL;
+  if (!n.ok) return MRF_ECUDA;
+  return n.comm_destroy(comm) == 0 ? MRF_OK : MRF_ECUDA;
+}
+
+int mrf_allreduce_grads_f32(void* nccl_comm, float* buffer, size_t count, cudaStream_t stream) {
+  const Nccl& n = nccl();
+  if (!nccl_comm || !buffer) return MRF_EINVAL;
+  if (!n.ok) return MRF_ECUDA;
+  // ncclAllReduce(sendbuff, recvbuff, count, ncclFloat32 = 7, ncclSum = 0, comm, stream), in place
+  return n.all_reduce(buffer, buffer, count, 7, 0, nccl_comm, stream) == 0 ? MRF_OK : MRF_ECUDA;
 }
 
 }  // extern "C"

@@ -88,38 +88,46 @@ def random_problem(H, W, L, conn, seed, per_edge=False, explicit=True, w_const=N
     return un, V, wc, planes
 
 
-def config(name: str, batch: int | None = None, engine: str | None = None) -> Workload:
-    """Full-size workload for configs C1..C5 (engine override for C5)."""
+def config(name: str, batch: int | None = None, engine: str | None = None, first: int = 0,
+           seed_offset: int = 0) -> Workload:
+    """Full-size workload for configs C1..C5 (engine override for C5).
+    C4: images first .. first+batch-1 of the seeded batch (a rank's shard;
+    the pairwise table is shared by every image). seed_offset gives C1-C3 and
+    C5 a different image per rank (weak scaling)."""
     name = name.upper()
     if name == "C1":
         H, W, L = 288, 384, 16
-        return Workload("C1", "isgmr", H, W, L, 4, 5, 1, stereo_like(H, W, L, 1)[None], truncated_linear(L, 2.0))
+        return Workload("C1", "isgmr", H, W, L, 4, 5, 1, stereo_like(H, W, L, 1 + seed_offset)[None],
+                        truncated_linear(L, 2.0))
     if name == "C2":
         H, W, L = 375, 1242, 192
-        return Workload("C2", "trwp", H, W, L, 4, 5, 1, stereo_like(H, W, L, 2)[None], truncated_linear(L, 2.0))
+        return Workload("C2", "trwp", H, W, L, 4, 5, 1, stereo_like(H, W, L, 2 + seed_offset)[None],
+                        truncated_linear(L, 2.0))
     if name == "C3":
         H, W, L = 500, 750, 128
-        return Workload("C3", "isgmr", H, W, L, 8, 5, 1, stereo_like(H, W, L, 3)[None], truncated_linear(L, 2.0))
+        return Workload("C3", "isgmr", H, W, L, 8, 5, 1, stereo_like(H, W, L, 3 + seed_offset)[None],
+                        truncated_linear(L, 2.0))
     if name == "C4":
         B = 32 if batch is None else batch
-        return seg_batch(512, 512, 21, B, seed0=100)
+        return seg_batch(512, 512, 21, B, seed0=100, first=first)
     if name == "C5":
         eng = engine or "isgmr"
         H = W = 512
         L = 256
-        un = denoise_tq(H, W, L, seed=5)
+        un = denoise_tq(H, W, L, seed=5 + seed_offset)
         return Workload("C5", eng, H, W, L, 4, 10, 1, un[None], truncated_quadratic(L, 200.0), w_const=25.0)
     raise ValueError(name)
 
 
-def seg_batch(H, W, L, B, seed0=100, conn=4, K=5) -> Workload:
+def seg_batch(H, W, L, B, seed0=100, conn=4, K=5, first=0) -> Workload:
     """C4: unary = -logits, logits ~ N(0, 3^2); V explicit U[0,2) with zero
     diagonal (gradcheck.hpp:51-55 recipe); per-edge weights 1 - |e_i - e_j|
-    from a seeded binary edge map."""
+    from a seeded binary edge map. Image b of the batch
+    is seeded seed0 + b; this returns images first .. first+B-1."""
     un = np.empty((B, H * W * L), np.float32)
     planes = np.empty((B, (conn // 2) * H * W), np.float32)
     for b in range(B):
-        rng = np.random.default_rng(seed0 + b)
+        rng = np.random.default_rng(seed0 + first + b)
         un[b] = (-rng.normal(0.0, 3.0, H * W * L)).astype(np.float32)
         e = (rng.uniform(size=(H, W)) < 0.1).astype(np.float32)
         pl = np.ones((conn // 2, H, W), np.float32)

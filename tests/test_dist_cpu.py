@@ -89,3 +89,19 @@ def test_gloo_world2_allreduce_matches_single_process():
     for rank in range(2):
         got = out[rank]
         assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_seg_batch_shards_are_slices_of_the_batch():
+    """A rank's C4 shard (workloads.seg_batch(first=...)) holds exactly the
+    images the single-process batch holds at those positions, with the same
+    shared pairwise table (bench.py --config C4 under torchrun)."""
+    from paper_1910_10892_b200 import workloads as WL
+
+    full = WL.seg_batch(12, 10, 5, 7)
+    for world in (2, 3, 4):
+        for rank in range(world):
+            a, b = shard_range(7, rank, world)
+            part = WL.seg_batch(12, 10, 5, b - a, first=a)
+            assert np.array_equal(part.unary, full.unary[a:b])
+            assert np.array_equal(part.w_planes, full.w_planes[a:b])
+            assert np.array_equal(part.V, full.V)

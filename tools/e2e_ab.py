@@ -8,6 +8,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_1910_10892_b200 import api  # noqa: E402
+from paper_1910_10892_b200.dist import DataParallelStep  # noqa: E402
 from paper_1910_10892_b200 import workloads as WL  # noqa: E402
 
 wl = WL.config(sys.argv[1] if len(sys.argv) > 1 else "C2")
@@ -18,7 +19,6 @@ unary = torch.from_numpy(wl.unary.reshape(wl.B, wl.N, wl.L)).to(dev)
 V = torch.from_numpy(wl.V.reshape(wl.L, wl.L)).to(dev)
 w = wl.w_const if wl.w_planes is None else torch.from_numpy(wl.w_planes.reshape(wl.B, wl.conn // 2, wl.N)).to(dev)
 fwd0 = api.isgmr_forward if wl.engine == "isgmr" else api.trwp_forward
-bwd0 = api.isgmr_backward if wl.engine == "isgmr" else api.trwp_backward
 LU = wl.K * topo.total_edges * wl.L
 
 
@@ -29,13 +29,12 @@ class A:
 pack0 = api.pack_shared_grads
 for v in variants * 2:
     mrf = api.MRF(topo, unary, V, w, wl.rho_const)
-    fwd_out = api._alloc_forward(mrf, wl.K)
-    fwd0(mrf, wl.K, out=fwd_out)
-    grads = api.GradientSet(torch.empty_like(unary), torch.empty((wl.B, wl.L, wl.L), device=dev),
-                            torch.empty((wl.B, wl.conn // 2, wl.N), device=dev))
-    shared = torch.empty(wl.L * wl.L + 1, device=dev)
-    fwd_fn = (lambda m, K, out: fwd_out) if v == "nofwd" else fwd0
-    bwd_fn = (lambda *a, **k: None) if v == "nobwd" else bwd0
+    dp = DataParallelStep(mrf, wl.engine, wl.K)
+    fwd0(mrf, wl.K, out=dp.fwd)
+    if v == "nofwd":
+        dp.forward = lambda mrf=None, out=None: dp.fwd
+    if v == "nobwd":
+        dp.backward = lambda *a, **k: None
     api.pack_shared_grads = (lambda *a, **k: None) if v in ("nopack", "nobwd") else pack0
-    r = bench.run_e2e(A, wl, mrf, fwd_fn, bwd_fn, fwd_out, grads, shared, 1, dev, LU, lambda: None)
+    r = bench.run_e2e(A, wl, mrf, dp, 1, wl.B, dev, LU, lambda: None)
     print(f"{v:8s} e2e ms/step {r['ms_per_step']:.3f}", flush=True)

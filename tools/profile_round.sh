@@ -1,30 +1,51 @@
 #!/bin/bash
 # Profile capture for profiles/ (run under gpurun; one GPU, never multi-rank).
-#   bash tools/profile_round.sh <tag>
-# 1) launch list of one C2 fwd+bwd (device time per launch, clocks unlocked)
-# 2) ncu --set full of the top kernels: first horizontal + vertical forward
-#    sweep and backward sweep launches of C2 (the banded-mode instantiation)
-# 3) the bench line itself (not under ncu; run first, see below)
+#   bash tools/profile_round.sh <tag> [configs...]     (default: C2 C4 C5 C3 C1)
+# 1) the bench line (not under ncu; run first: a bench right after the ncu
+#    replays measured 10-50% slow on the same box in round 1)
+# 2) per config: the launch list of one fwd+bwd (device time per launch,
+#    clocks unlocked) and ncu --set full of the top kernels, summarised with
+#    pipe-utilisation counters and per-edge / per-chain-step models
+#    (tools/ncu_summary.py). The .ncu-rep files stay on the box.
 set -x
-TAG=${1:-r01}
+TAG=${1:-r02}
+shift
+CONFIGS=${@:-C2 C4 C5 C3 C1}
 mkdir -p gpurun_out
-# the bench line first: a bench run right after the ncu replays measured
-# 10-50% slow on the same box (r01e, r01h), never on a fresh one
 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_C2_${TAG}.json 2> gpurun_out/bench_C2_${TAG}.err
 tail -1 gpurun_out/bench_C2_${TAG}.json
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2_${TAG}.csv \
-    python tools/prof_run.py C2 1 > /dev/null 2>&1
 NCU="ncu --set full --import-source on --clock-control none --kernel-name-base demangled"
-# forward: directions E, W (horizontal), S, N (vertical) per iteration -> launch 0 = H, 2 = V
-$NCU -k regex:fwd_band2_kernel -s 0 -c 1 -o gpurun_out/ncu_fwdH_C2_${TAG} python tools/prof_run.py C2 1 > /dev/null 2>&1
-$NCU -k regex:fwd_band2_kernel -s 2 -c 1 -o gpurun_out/ncu_fwdV_C2_${TAG} python tools/prof_run.py C2 1 > /dev/null 2>&1
-# backward: directions N, S (vertical), W, E (horizontal), each as 3 launches (banded D<=2,
-# window, general; the non-owners exit at once): launch 0 = N (vertical), 6 = W (horizontal)
-$NCU -k regex:bwd_split_kernel -s 0 -c 1 -o gpurun_out/ncu_bwdV_C2_${TAG} python tools/prof_run.py C2 1 > /dev/null 2>&1
-$NCU -k regex:bwd_split_kernel -s 6 -c 1 -o gpurun_out/ncu_bwdH_C2_${TAG} python tools/prof_run.py C2 1 > /dev/null 2>&1
-# summaries for profiles/ (the .ncu-rep files stay on the box: gpurun brings back <= 64 MiB)
-for k in fwdH fwdV bwdH bwdV; do
-  python tools/ncu_summary.py full gpurun_out/ncu_${k}_C2_${TAG}.ncu-rep gpurun_out/ncu_${k}_C2_${TAG}.json "C2 $k ${TAG}"
+cap() {  # cap <cfg> <name> <kernel regex> <skip> <edges> <longest line steps>
+  local cfg=$1 name=$2 kre=$3 skip=$4 edges=$5 steps=$6
+  $NCU -k "regex:$kre" -s $skip -c 1 -o gpurun_out/ncu_${name}_${cfg}_${TAG} python tools/prof_run.py $cfg 1 > /dev/null 2>&1
+  python tools/ncu_summary.py full gpurun_out/ncu_${name}_${cfg}_${TAG}.ncu-rep gpurun_out/ncu_${name}_${cfg}_${TAG}.json \
+    "$cfg $name $TAG" $edges $steps
+  rm -f gpurun_out/ncu_${name}_${cfg}_${TAG}.ncu-rep
+}
+for CFG in $CONFIGS; do
+  export PROF_BATCH=
+  [ "$CFG" = C4 ] && export PROF_BATCH=32
+  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${CFG}_${TAG}.csv \
+      python tools/prof_run.py $CFG 1 > /dev/null 2>&1
+  python tools/ncu_summary.py launches gpurun_out/launches_${CFG}_${TAG}.csv gpurun_out/launches_${CFG}_${TAG}.json
+  case $CFG in
+    C2)  # TRWP-4 375x1242: forward launch 0 = E (horizontal), 2 = S (vertical); backward
+         # sweeps N, S, W, E with 3 strategy launches each: 0 = N (vertical), 6 = W (horizontal)
+      cap C2 fwdH fwd_band2_kernel 0 465375 1241
+      cap C2 fwdV fwd_band2_kernel 2 464508 374
+      cap C2 bwdV bwd_split_kernel 0 464508 374
+      cap C2 bwdH bwd_split_kernel 6 465375 1241 ;;
+    C4)  # TRWP-4 512x512 L=21, B=32: one launch covers the batch
+      cap C4 fwd fwd_small_kernel 0 8372224 511
+      cap C4 bwd bwd_small_kernel 0 8372224 511 ;;
+    C5)  # ISGMR-4 512x512 L=256 TQ: one launch per iteration over all directions
+      cap C5 fwd fwd_bandw_kernel 0 1046528 511
+      cap C5 bwd "bwd_split_kernel<8, false, 4, true, 3, 2>" 0 1046528 511 ;;
+    C3)  # ISGMR-8 500x750 L=128
+      cap C3 fwd fwd_band2_kernel 0 2992504 749
+      cap C3 bwd bwd_split_kernel 0 2992504 749 ;;
+    C1)
+      cap C1 fwd fwd_band2_kernel 0 441024 383
+      cap C1 bwd bwd_ 0 441024 383 ;;
+  esac
 done
-python tools/ncu_summary.py launches gpurun_out/launches_C2_${TAG}.csv gpurun_out/launches_C2_${TAG}.json
-rm -f gpurun_out/*.ncu-rep
