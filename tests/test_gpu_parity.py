@@ -334,3 +334,4 @@ def test_non_finite_unary_rejected_at_the_c_abi(engine):
         mrf.assume_finite = True  # caller's promise: no scan, no error
         fwd(mrf, 1)
         torch.cuda.synchronize()
+
