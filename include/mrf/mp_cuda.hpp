@@ -836,6 +836,104 @@ double energy(const GridTopology& topo, const PotentialSet<Real>& pots, const st
   return e;
 }
 
+/// baselines.hpp:16-24
+enum class SgmVariant { standard, revised };
+
+template <class Real>
+struct SgmResult {
+  CostOutput<Real> output;
+  std::vector<Real> messages;  // R*N*L
+};
+
+namespace cuda_detail {
+
+// One SGM round on uploaded potentials (mrf_sgm_f32), results left on the device.
+struct SgmRound {
+  DeviceBuffer msg, cost, labels;
+};
+
+inline SgmRound sgm_round(const GridTopology& topo, const mrf_problem_f32& prob, SgmVariant variant) {
+  const size_t n = size_t(topo.grid().nodes()), L = size_t(prob.labels), R = size_t(topo.num_dirs());
+  SgmRound rd{DeviceBuffer(sizeof(float) * R * n * L), DeviceBuffer(sizeof(float) * n * L), DeviceBuffer(2 * n)};
+  check(mrf_sgm_f32(topo.handle(), &prob, variant == SgmVariant::revised ? 1 : 0, rd.msg.as<float>(),
+                    rd.cost.as<float>(), rd.labels.as<std::uint16_t>(), nullptr));
+  return rd;
+}
+
+inline CostOutput<float> download_cost(const GridTopology& topo, int L, const SgmRound& rd) {
+  const size_t n = size_t(topo.grid().nodes());
+  CostOutput<float> out;
+  out.height = topo.grid().height;
+  out.width = topo.grid().width;
+  out.labels = L;
+  out.cost.resize(n * L);
+  out.labels_map.resize(n);
+  rd.cost.download(out.cost.data(), out.cost.size());
+  rd.labels.download(out.labels_map.data(), n);
+  return out;
+}
+
+}  // namespace cuda_detail
+
+/// baselines.hpp:31-98
+template <class Real>
+SgmResult<Real> sgm_forward(const GridTopology& topo, const PotentialSet<Real>& pots, SgmVariant variant,
+                            int threads = 1) {
+  cuda_detail::require_float<Real>();
+  (void)threads;
+  auto d = cuda_detail::upload(topo, pots, nullptr, false);
+  const auto rd = cuda_detail::sgm_round(topo, d.prob, variant);
+  SgmResult<float> res;
+  res.output = cuda_detail::download_cost(topo, d.prob.labels, rd);
+  res.messages.resize(size_t(topo.num_dirs()) * topo.grid().nodes() * d.prob.labels);
+  rd.msg.download(res.messages.data(), res.messages.size());
+  return res;
+}
+
+/// baselines.hpp:108-145: each round's unary volume is the previous round's
+/// message sum, per-node minimum subtracted (mrf_sgm_next_unary_f32); the
+/// volume stays on the device between rounds.
+template <class Real>
+class SgmIterative {
+ public:
+  SgmIterative(const GridTopology& topo, const PotentialSet<Real>& pots, SgmVariant variant = SgmVariant::standard,
+               int threads = 1)
+      : topo_(topo), d_((cuda_detail::require_float<Real>(), cuda_detail::upload(topo, pots, nullptr, false))),
+        variant_(variant) {
+    (void)threads;
+  }
+
+  const CostOutput<Real>& step() {
+    const auto rd = cuda_detail::sgm_round(topo_, d_.prob, variant_);
+    last_ = cuda_detail::download_cost(topo_, d_.prob.labels, rd);
+    cuda_detail::DeviceBuffer next(sizeof(float) * size_t(topo_.grid().nodes()) * d_.prob.labels);
+    cuda_detail::check(mrf_sgm_next_unary_f32(topo_.handle(), &d_.prob, rd.msg.as<float>(), next.as<float>(), nullptr));
+    d_.unary = std::move(next);
+    d_.prob.unary = d_.unary.as<float>();
+    return last_;
+  }
+
+  const CostOutput<Real>& last() const { return last_; }
+
+ private:
+  const GridTopology& topo_;
+  cuda_detail::DeviceProblem d_;
+  SgmVariant variant_;
+  CostOutput<Real> last_;
+};
+
+/// baselines.hpp:147-161
+template <class Real>
+std::vector<CostOutput<Real>> sgm_iterative(const GridTopology& topo, const PotentialSet<Real>& pots, int iterations,
+                                            SgmVariant variant = SgmVariant::standard, int threads = 1) {
+  if (iterations < 1) throw std::invalid_argument("sgm_iterative: iterations must be >= 1");
+  SgmIterative<Real> it(topo, pots, variant, threads);
+  std::vector<CostOutput<Real>> out;
+  out.reserve(iterations);
+  for (int k = 0; k < iterations; ++k) out.push_back(it.step());
+  return out;
+}
+
 /// isgmr.hpp:156-169: energy of the aggregated labelling after each
 /// iteration, optionally on a separate evaluation topology (the 4-connected
 /// protocol).

@@ -222,6 +222,14 @@ int mrf_energy_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const uint1
 int mrf_sgm_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int variant, float* messages, float* cost,
                 uint16_t* labels, cudaStream_t stream);
 
+/* Iterated SGM (mp::SgmIterative::step, baselines.hpp:108-161): after a
+ * mrf_sgm_f32 round, the next round's unary volume from that round's
+ * messages: next(i, l) = sum_r m^r(i, l) - min_l' sum_r m^r(i, l') (r
+ * ascending). messages [B][R][N][L], next_unary [B][N][L] (device, must not
+ * alias messages). Stream-ordered. */
+int mrf_sgm_next_unary_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const float* messages, float* next_unary,
+                           cudaStream_t stream);
+
 /* ---------------------------------------------------------- instrumentation */
 
 /* Kernel classes for the launch profiler. */

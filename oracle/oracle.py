@@ -100,6 +100,7 @@ def _ref():
         lib.ref_sgm_revised_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp]
         lib.ref_energy_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp]
         lib.ref_sgm_standard_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, _vp, _vp, _vp]
+        lib.ref_sgm_iterative_f32.argtypes = [C.c_int] * 4 + [_vp, _vp, C.c_float, _vp, C.c_int, C.c_int, _vp, _vp]
         lib.ref_gradient_check.argtypes = [C.c_int] * 7 + [C.c_uint64, _vp, _vp, _vp]
         lib._typed = True
     return lib
@@ -319,6 +320,16 @@ def ref_sgm_standard(pr: Problem):
     _check_ref(_ref().ref_sgm_standard_f32(pr.H, pr.W, pr.L, pr.conn, _ptr(pr.unary), _ptr(pr.V), pr.w_const,
                                            _ptr(pr.w_planes), _ptr(cost), _ptr(labels), _ptr(msg)))
     return cost, labels, msg
+
+
+def ref_sgm_iterative(pr: Problem, K: int, variant: str = "standard"):
+    """mp::sgm_iterative of the reference: [(cost, labels)] per round."""
+    costs = np.zeros((K, pr.N * pr.L), np.float32)
+    labels = np.zeros((K, pr.N), np.uint16)
+    _check_ref(_ref().ref_sgm_iterative_f32(pr.H, pr.W, pr.L, pr.conn, _ptr(pr.unary), _ptr(pr.V), pr.w_const,
+                                            _ptr(pr.w_planes), K, int(variant == "revised"), _ptr(costs),
+                                            _ptr(labels)))
+    return [(costs[k], labels[k]) for k in range(K)]
 
 
 def ref_energy(pr: Problem, labels) -> float:

@@ -249,6 +249,23 @@ REF_API int ref_sgm_standard_f32(int H, int W, int L, int conn, const float* una
   });
 }
 
+/// Iterated SGM (baselines.hpp:108-161): per round cost [K][N][L] and labels [K][N].
+REF_API int ref_sgm_iterative_f32(int H, int W, int L, int conn, const float* unary, const float* table,
+                                  float w_const, const float* w_planes, int iterations, int variant, float* costs,
+                                  uint16_t* labels) {
+  return guarded([&] {
+    const auto topo = make_topo(H, W, conn);
+    const auto pots = make_pots<float>(H, W, L, conn, unary, table, w_const, w_planes);
+    const auto out = mp::sgm_iterative(topo, pots, iterations,
+                                       variant ? mp::SgmVariant::revised : mp::SgmVariant::standard, 1);
+    const size_t nl = size_t(H) * W * L, n = size_t(H) * W;
+    for (size_t k = 0; k < out.size(); ++k) {
+      std::memcpy(costs + k * nl, out[k].cost.data(), sizeof(float) * nl);
+      std::memcpy(labels + k * n, out[k].labels_map.data(), sizeof(uint16_t) * n);
+    }
+  });
+}
+
 /// Energy of a labelling (potentials.hpp:175-199), double accumulation.
 REF_API int ref_energy_f32(int H, int W, int L, int conn, const float* unary, const float* table,
                            float w_const, const float* w_planes, const uint16_t* labels, double* out) {

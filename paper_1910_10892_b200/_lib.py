@@ -71,6 +71,7 @@ SIGNATURES = {
     "mrf_soft_head_f32": (_i, [_i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "mrf_energy_f32": (_i, [_vp, _PP, _vp, C.POINTER(C.c_double), _vp]),
     "mrf_sgm_f32": (_i, [_vp, _PP, _i, _vp, _vp, _vp, _vp]),
+    "mrf_sgm_next_unary_f32": (_i, [_vp, _PP, _vp, _vp, _vp]),
     "mrf_profiler_enable": (_i, [_i]),
     "mrf_profiler_read": (_i, [_i, C.POINTER(C.c_double), _i64p]),
     "mrf_launch_count": (_i, [_i64p]),

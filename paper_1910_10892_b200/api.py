@@ -454,6 +454,25 @@ def iterate_energy(engine: str, mrf: MRF, iterations: int, eval_topo: GridTopolo
     return out
 
 
+def sgm_iterative(mrf: MRF, iterations: int, variant: str = "standard", stream=None):
+    """mp::sgm_iterative (baselines.hpp:108-161): `iterations` SGM rounds,
+    each on the previous round's normalised message sum as its unary volume.
+    Returns [(cost [B,N,L], labels [B,N] int16)] per round."""
+    if iterations < 1:
+        raise _lib.MrfInvalidArgument(1, "sgm_iterative: iterations must be >= 1")
+    cur = MRF(mrf.topo, mrf.unary, mrf.V, mrf.weight, mrf.rho, mrf.assume_finite)
+    out = []
+    for k in range(iterations):
+        cost, labels, msgs = sgm_forward(cur, variant, stream)
+        out.append((cost, labels))
+        if k + 1 < iterations:
+            nxt = torch.empty_like(mrf.unary)
+            pr = cur.c_problem()
+            check(lib().mrf_sgm_next_unary_f32(cur.topo.handle, C.byref(pr), _ptr(msgs), _ptr(nxt), _stream(stream)))
+            cur = MRF(mrf.topo, nxt, mrf.V, mrf.weight, mrf.rho, True)
+    return out
+
+
 def sgm_forward(mrf: MRF, variant: str = "standard", stream=None):
     """mp::sgm_forward (baselines.hpp:31-98): returns (cost [B,N,L], labels
     [B,N] int16, messages [B,R,N,L]). 'revised' is one ISGMR iteration."""
@@ -465,3 +484,46 @@ def sgm_forward(mrf: MRF, variant: str = "standard", stream=None):
     pr = mrf.c_problem()
     check(lib().mrf_sgm_f32(t.handle, C.byref(pr), v, _ptr(msgs), _ptr(cost), _ptr(labels), _stream(stream)))
     return cost, labels, msgs
+
+
+# ------------------------------------------------------------------ MPCV1 I/O
+
+_MPCV1 = b"MPCV1"
+
+
+def save_cost_volume(path: str, volume) -> None:
+    """Write an [H, W, L] float32 cost volume as MPCV1 (the reference's
+    on-disk format, io.hpp:29-35 / io.cpp:118-131): magic, H, W, L as
+    little-endian uint32, then the values row-major with label fastest."""
+    import numpy as np
+
+    v = volume.detach().cpu().numpy() if isinstance(volume, torch.Tensor) else np.asarray(volume)
+    if v.ndim != 3:
+        raise _lib.MrfInvalidArgument(1, "cost volume: expected [H, W, L]")
+    H, W, L = v.shape
+    with open(path, "wb") as f:
+        f.write(_MPCV1 + np.array([H, W, L], "<u4").tobytes() + np.ascontiguousarray(v, "<f4").tobytes())
+
+
+def load_cost_volume(path: str):
+    """Read an MPCV1 cost volume as a float32 numpy [H, W, L] array, with the
+    reference reader's checks (io.cpp:133-152): magic, non-zero sizes,
+    L <= 256, complete payload, finite values."""
+    import numpy as np
+
+    with open(path, "rb") as f:
+        raw = f.read()
+    if raw[:5] != _MPCV1:
+        raise ValueError(f"cost volume: bad magic in {path}")
+    if len(raw) < 17:
+        raise ValueError("cost volume: truncated header")
+    H, W, L = (int(x) for x in np.frombuffer(raw[5:17], "<u4"))
+    if not (H and W and L) or L > 256:
+        raise ValueError("cost volume: invalid dimensions")
+    n = H * W * L
+    if len(raw) < 17 + 4 * n:
+        raise ValueError("cost volume: truncated payload")
+    v = np.frombuffer(raw[17:17 + 4 * n], "<f4").astype(np.float32).reshape(H, W, L)
+    if not np.isfinite(v).all():
+        raise ValueError("cost volume: non-finite value")
+    return v

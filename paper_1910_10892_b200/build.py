@@ -57,8 +57,31 @@ def _compile(unit: str):
     return obj, res.stderr
 
 
+CLI_SRC = os.path.join(HERE, "cli", "mrfmp_cuda.cpp")
+CLI_OUT = os.path.join(HERE, "bin", "mrfmp_cuda")
+CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+
+
+def build_cli() -> str:
+    """The reference CLI's `run` driver over the C++ drop-in header
+    (cli/mrfmp_cuda.cpp), linked against the in-tree libmrf_cuda.so."""
+    deps = [CLI_SRC, OUT, os.path.join(ROOT, "include", "mrf", "mp_cuda.hpp"), os.path.join(ROOT, "include", "mrf", "io.hpp")]
+    if os.path.exists(CLI_OUT) and all(os.path.getmtime(d) <= os.path.getmtime(CLI_OUT) for d in deps):
+        return CLI_OUT
+    os.makedirs(os.path.dirname(CLI_OUT), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", os.path.join(CUDA_HOME, "include"),
+           CLI_SRC, "-o", CLI_OUT + ".tmp", "-L", HERE, "-lmrf_cuda", "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart",
+           "-Wl,-rpath,$ORIGIN/..:" + os.path.join(CUDA_HOME, "lib64")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("CLI build failed:\n" + " ".join(cmd) + "\n" + res.stdout + res.stderr)
+    os.replace(CLI_OUT + ".tmp", CLI_OUT)
+    return CLI_OUT
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        build_cli()
         return OUT
     os.makedirs(OBJDIR, exist_ok=True)
     workers = max(1, min(len(UNITS), os.cpu_count() or 1))
@@ -74,6 +97,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("".join(log for _, log in results))
     if verbose:
         print("".join(log for _, log in results), file=sys.stderr)
+    build_cli()
     return OUT
 
 

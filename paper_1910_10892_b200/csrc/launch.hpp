@@ -49,6 +49,7 @@ cudaError_t launch_energy(int B, int H, int W, int L, int R, const EvenSteps& st
                           float w, const float* wplanes, const uint16_t* labels, double* out, double* partial, int nblk,
                           int* bad, cudaStream_t s);
 int energy_blocks(int N);
+cudaError_t launch_sgm_next_unary(int B, int N, int L, int R, const float* messages, float* next, cudaStream_t s);
 cudaError_t launch_sgm_standard(const Geometry& g, const Potentials& pot, const LineDesc* lines, int nlines, float* m,
                                 int batch, cudaStream_t s);
 

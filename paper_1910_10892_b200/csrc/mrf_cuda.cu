@@ -731,6 +731,18 @@ int mrf_sgm_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int variant, f
   });
 }
 
+int mrf_sgm_next_unary_f32(mrf_topology_t topo, const mrf_problem_f32* prob, const float* messages, float* next_unary,
+                           cudaStream_t stream) {
+  return guarded([&] {
+    validate_problem(topo, prob);
+    if (!messages || !next_unary) fail(MRF_EINVAL, "sgm_next_unary: null messages or output");
+    ProfScope ps(stream, MRF_KCLASS_AUX);
+    cuda_check(launch_sgm_next_unary(prob->batch, topo->host.nodes(), prob->labels, topo->host.num_dirs(), messages,
+                                     next_unary, stream),
+               "sgm_next_unary launch");
+  });
+}
+
 int mrf_profiler_enable(int on) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_prof.mu);

@@ -98,7 +98,46 @@ cudaError_t run(const Geometry& g, const Potentials& pot, const LineDesc* lines,
   return cudaGetLastError();
 }
 
+// Iterated SGM's unary update (baselines.hpp:120-134): s(l) = sum_r m^r(l)
+// (r ascending from +0), lo = min_l s(l) (std::min from +inf: first of equal
+// values), next(l) = s(l) - lo. One warp per node.
+__global__ void __launch_bounds__(256) sgm_next_unary_kernel(int N, int L, int R, const float* __restrict__ m,
+                                                              float* __restrict__ next) {
+  const int lane = threadIdx.x & 31;
+  const int64_t node = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int b = blockIdx.y;
+  if (node >= N) return;
+  const float* mb = m + size_t(b) * R * N * L + size_t(node) * L;
+  float* nb = next + (size_t(b) * N + node) * L;
+  float s[8];
+  float lo = kInf;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int l = lane + 32 * i;
+    s[i] = 0.0f;
+    if (l < L) {
+      for (int r = 0; r < R; ++r) s[i] = fadd(s[i], __ldcs(mb + size_t(r) * N * L + l));
+      lo = s[i] < lo ? s[i] : lo;  // s is never -0 (+0 + x), so fminf order does not matter
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int l = lane + 32 * i;
+    if (l < L) nb[l] = fsub(s[i], lo);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_sgm_next_unary(int B, int N, int L, int R, const float* messages, float* next, cudaStream_t s) {
+  const int wpb = 8;
+  sgm_next_unary_kernel<<<dim3(unsigned((int64_t(N) + wpb - 1) / wpb), unsigned(B)), 32 * wpb, 0, s>>>(N, L, R, messages,
+                                                                                                      next);
+  note_launch();
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sgm_standard(const Geometry& g, const Potentials& pot, const LineDesc* lines, int nlines, float* m,
                                 int batch, cudaStream_t s) {

@@ -208,6 +208,34 @@ int main() {
     threw = true;
   }
   CHECK(threw);
+  // SGM baselines (baselines.hpp:31-161): revised == one ISGMR iteration
+  // (test_baselines.cpp:58-68); iterated SGM's first round is sgm_forward's
+  // and later rounds change the labelling's input (exact parity with the
+  // reference library: tests/test_gpu_head.py)
+  {
+    const int H = 7, W = 8, L = 6;
+    std::mt19937 rng(5);
+    std::uniform_real_distribution<float> U(0.f, 6.f);
+    PotentialSet<float> pots;
+    pots.unary = UnaryVolume<float>(H, W, L);
+    for (auto& v : pots.unary.values) v = U(rng);
+    pots.pairwise = build_pairwise<float>(PairwiseKind::truncated_linear, {2.0, 1.0, 1.0}, L);
+    const GridTopology t4(GridGraph(H, W), DirectionSet::build(4));
+    const auto rev = sgm_forward(t4, pots, SgmVariant::revised);
+    const auto one = isgmr_forward(t4, pots, 1);
+    CHECK(rev.output.cost == one.output.cost && rev.messages == one.messages);
+    const auto std1 = sgm_forward(t4, pots, SgmVariant::standard);
+    const auto it = sgm_iterative(t4, pots, 3);
+    CHECK(it.size() == 3 && it[0].cost == std1.output.cost && it[0].labels_map == std1.output.labels_map);
+    CHECK(it[1].cost != it[0].cost);
+    bool threw = false;
+    try {
+      sgm_iterative(t4, pots, 0);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+  }
   // readout and evaluation (softhead.hpp:22-74, potentials.hpp:175-199)
   {
     const int H = 6, W = 7, L = 9;

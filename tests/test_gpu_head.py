@@ -140,3 +140,21 @@ def test_sgm_matches_reference(H, W, L, conn, per_edge, explicit):
     assert np.array_equal(labels[0].cpu().numpy().view(np.uint16), l_ref)
     c_rev, _ = O.ref_sgm_revised(pr)
     assert np.array_equal(c_rev.view(np.uint32), ref.cost.view(np.uint32))
+
+
+@pytest.mark.parametrize("variant", ["standard", "revised"])
+@pytest.mark.parametrize("H,W,L,conn,per_edge,explicit", [(6, 7, 5, 4, False, True), (9, 8, 16, 8, True, False),
+                                                          (7, 9, 21, 4, True, True)])
+def test_sgm_iterative_matches_reference(variant, H, W, L, conn, per_edge, explicit):
+    """mp::sgm_iterative (baselines.hpp:108-161): every round's cost and
+    labels bit-identical to the reference library's."""
+    if not O.have_ref():
+        pytest.skip("reference library not present")
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=H + W * L, per_edge=per_edge, explicit=explicit)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    K = 4
+    got = api.sgm_iterative(to_mrf(pr), K, variant)
+    want = O.ref_sgm_iterative(pr, K, variant)
+    for k in range(K):
+        assert np.array_equal(got[k][0][0].cpu().numpy().reshape(-1).view(np.uint32), want[k][0].view(np.uint32)), k
+        assert np.array_equal(got[k][1][0].cpu().numpy().view(np.uint16), want[k][1]), k
