@@ -184,61 +184,87 @@ def implemented_bytes(wl, E_r, dv_slots):
 
 # ---------------------------------------------------------------- cpu baseline
 
-def cpu_reference_sample(wl, budget_s: float = 12.0, rows: int | None = None):
-    """Reference library (oracle/_ref; restatement if absent) fwd+bwd on a
-    horizontal strip of the same workload, all host threads. Returns
-    (LU/s, seconds, sample description, kind, cores)."""
+def host_info(threads: int) -> dict:
+    """nproc, CPU model and OpenMP setting of the host the CPU legs ran on
+    (BASELINE.md §3 item 3)."""
+    model = None
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "threads_used": threads}
+
+
+def cpu_reference_run(wl, K: int, rows: int | None = None, threads: int = 0):
+    """One fwd+bwd of the reference library (oracle/_ref; the C restatement if
+    absent) on image 0 of the workload, rows [0, rows) (default: the whole
+    image), K iterations, `threads` OpenMP threads (0 = all). Returns
+    (label-updates, seconds, kind)."""
     from oracle import oracle as O
 
     kind = "reference" if O.have_ref() else "port"
     impl = "ref" if kind == "reference" else "oracle"
-    cores = os.cpu_count() if kind == "reference" else 1
-    K = 1  # one of the K identical iterations; LU scales linearly in K
+    h = wl.H if rows is None else rows
+    un = wl.unary[0].reshape(wl.H, wl.W * wl.L)[:h].reshape(-1).copy()
+    wp = None
+    if wl.w_planes is not None:
+        wp = wl.w_planes[0].reshape(wl.conn // 2, wl.H, wl.W)[:, :h].reshape(-1).copy()
+    pr = O.Problem(h, wl.W, wl.L, wl.conn, un, wl.V, wl.w_const, wp, wl.rho_const, None)
+    E = O.total_edges(h, wl.W, wl.conn)
+    gc = np.full(h * wl.W * wl.L, 1.0 / (h * wl.W * wl.L), np.float32)
+    t0 = time.perf_counter()
+    f = O.forward(wl.engine, pr, K, impl=impl, threads=threads)
+    O.backward(wl.engine, pr, K, f.p, f.q, gc, impl=impl, threads=threads)
+    return K * E * wl.L, time.perf_counter() - t0, kind
 
-    def run(h):
-        un = wl.unary[0].reshape(wl.H, wl.W * wl.L)[:h].reshape(-1).copy()
-        wp = None
-        if wl.w_planes is not None:
-            wp = wl.w_planes[0].reshape(wl.conn // 2, wl.H, wl.W)[:, :h].reshape(-1).copy()
-        pr = O.Problem(h, wl.W, wl.L, wl.conn, un, wl.V, wl.w_const, wp, wl.rho_const, None)
-        E = O.total_edges(h, wl.W, wl.conn)
-        gc = np.full(h * wl.W * wl.L, 1.0 / (h * wl.W * wl.L), np.float32)
-        t0 = time.perf_counter()
-        f = O.forward(wl.engine, pr, K, impl=impl, threads=0)
-        O.backward(wl.engine, pr, K, f.p, f.q, gc, impl=impl, threads=0)
-        dt = time.perf_counter() - t0
-        return K * E * wl.L, dt
 
-    if rows is None:
-        lu, dt = run(min(8, wl.H))
-        rows = int(min(wl.H, max(2, 8 * budget_s / max(dt, 1e-3))))
-    lu, dt = run(rows)
-    desc = (f"{wl.name} {wl.engine.upper()}-{wl.conn} strip rows[0:{rows}] x {wl.W}, L={wl.L}, K=1 of {wl.K} "
-            f"(per-iteration work identical), fwd+bwd, OpenMP threads={cores}")
-    return lu / dt, dt, desc, kind, cores, rows
+def cpu_baseline(wl) -> dict:
+    """bench.py's cpu_baseline leg: the reference library on
+    this host, the WHOLE image at the full K (no extrapolation; the
+    reference's O(K^2) index-store regrowth included), all host threads; plus
+    a 1-thread figure on a strip of the image at K = 1 (same per-row work)."""
+    lu, dt, kind = cpu_reference_run(wl, wl.K)
+    rows1 = max(2, min(wl.H, wl.H // 16))
+    lu1, dt1, _ = cpu_reference_run(wl, 1, rows=rows1, threads=1)
+    return {"value": lu / dt / 1e9, "unit": "G label-updates/s", "cores": os.cpu_count(), "kind": kind,
+            "sample": f"{wl.name} {wl.engine.upper()}-{wl.conn} image 0, all {wl.H}x{wl.W} nodes, L={wl.L}, "
+                      f"K={wl.K}, fwd+bwd, OpenMP threads=all ({os.cpu_count()}); not extrapolated",
+            "seconds": dt, "one_thread": {"value": lu1 / dt1 / 1e9, "seconds": dt1,
+                                          "sample": f"rows[0:{rows1}] x {wl.W}, K=1, fwd+bwd, 1 thread"},
+            "host": host_info(0)}
 
 
 # --------------------------------------------------------------------- runs
 
 def run_reference_arm(args, wl):
-    """--impl reference: the reference CPU implementation on the host cores."""
-    total_steps = args.steps + args.warmup
-    budget = max(2.0, 150.0 / max(total_steps, 1))
-    _, _, desc, kind, cores, rows = cpu_reference_sample(wl, budget_s=budget)
+    """--impl reference: the reference CPU implementation (oracle/_ref) on the
+    host cores. Every timed step is one fwd+bwd iteration (K = 1 of the
+    config's K identical iterations) over the WHOLE image with all host
+    threads -- the workload of one GPU step divided by K; the value is its
+    label-update rate. Warm-up steps run on an 8-row strip (paging in the
+    library and the inputs, untimed)."""
+    kind = None
+    for _ in range(args.warmup):
+        _, _, kind = cpu_reference_run(wl, 1, rows=min(8, wl.H))
     lus, dts = [], []
-    for i in range(total_steps):
-        lu_s, dt, desc, kind, cores, rows = cpu_reference_sample(wl, rows=rows)
-        if i >= args.warmup:
-            lus.append(lu_s * dt)
-            dts.append(dt)
+    for _ in range(args.steps):
+        lu, dt, kind = cpu_reference_run(wl, 1)
+        lus.append(lu)
+        dts.append(dt)
     value = sum(lus) / sum(dts) / 1e9
+    desc = (f"{wl.name} {wl.engine.upper()}-{wl.conn} image 0, all {wl.H}x{wl.W} nodes, L={wl.L}, one of the "
+            f"K={wl.K} iterations per step (per-iteration work identical), fwd+bwd, OpenMP threads=all")
     line = {
         "impl": "reference", "metric": metric_name(wl), "value": value, "unit": "G label-updates/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(dts) / len(dts), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_dict(wl, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "G label-updates/s", "cores": cores, "kind": kind,
-                         "sample": desc},
+        "ms_per_step": 1e3 * sum(dts) / len(dts), "ms_per_step_median": 1e3 * float(np.median(dts)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(wl, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "G label-updates/s", "cores": os.cpu_count(), "kind": kind,
+                         "sample": desc, "host": host_info(0)},
         "e2e": {"value": value, "unit": "G label-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -249,12 +275,27 @@ def metric_name(wl):
             f"(ms/image alongside)")
 
 
+def working_set_bytes(wl) -> int:
+    """Bytes one step touches per GPU: unary, messages, p, q."""
+    R, N, L, K = wl.conn, wl.N, wl.L, wl.K
+    E = sum((wl.H - abs(dh)) * (wl.W - abs(dw)) for dh, dw in
+            [(0, 1), (0, -1), (1, 0), (-1, 0), (1, 1), (-1, -1), (1, -1), (-1, 1)][:min(R, 8)]) if R <= 8 else N * R
+    return wl.B * (N * L * 4 * (R + 1) + K * E * (L + 1))
+
+
+def l2_flush_needed(wl) -> bool:
+    return working_set_bytes(wl) < 2 * 126 * 2 ** 20
+
+
 def config_dict(wl, n, global_batch=None):
     return {"workload": f"{wl.name}: {wl.engine.upper()} fwd+bwd, {wl.conn} directions, K={wl.K}, "
                         f"{wl.W}x{wl.H} synthetic volume, {wl.L} labels",
             "H": wl.H, "W": wl.W, "L": wl.L, "K": wl.K, "connectivity": wl.conn, "engine": wl.engine,
             "images_per_gpu": wl.B, "global_batch": global_batch or wl.B * n, "parallelism": f"dp{n}",
-            "l2": "inputs larger than L2 (unary, messages and indices each exceed 126 MB per image)"}
+            "l2": (f"L2 flushed (256 MB write) before every timed step: working set {working_set_bytes(wl) / 1e6:.0f} MB"
+                   if l2_flush_needed(wl) else
+                   f"inputs larger than L2: working set {working_set_bytes(wl) / 1e9:.2f} GB per GPU (unary, "
+                   f"messages, indices)")}
 
 
 def main():
@@ -329,12 +370,17 @@ def main():
     import ctypes as C
     n0 = C.c_int64()
     _lib.check(_lib.lib().mrf_launch_count(C.byref(n0)))
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
+    # a step's working set smaller than twice the L2 gets the L2 flushed
+    # (a 256 MB write, outside the per-step event pairs) before every step
+    flush = l2_flush_needed(wl)
+    scratch = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for a_ev, b_ev in evs:
+        if flush:
+            scratch.fill_(1)
+        a_ev.record(stream)
         step()
-    t1.record(stream)
+        b_ev.record(stream)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -342,7 +388,7 @@ def main():
     n1 = C.c_int64()
     _lib.check(_lib.lib().mrf_launch_count(C.byref(n1)))
     launches = n1.value - n0.value  # every kernel this library launched in the timed region
-    ms = t0.elapsed_time(t1)
+    ms = sum(a_ev.elapsed_time(b_ev) for a_ev, b_ev in evs)
     # per-kernel-class device time (roofline): a second pass of the same K
     # steps with the library's launch profiler on (events around every
     # launch), kept out of the timed region above
@@ -425,9 +471,7 @@ def main():
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        lu_s, dt, desc, kind, cores, _ = cpu_reference_sample(wl)
-        line["cpu_baseline"] = {"value": lu_s / 1e9, "unit": "G label-updates/s", "cores": cores, "kind": kind,
-                                "sample": desc, "seconds": dt}
+        line["cpu_baseline"] = cpu_baseline(wl)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
