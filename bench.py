@@ -418,7 +418,8 @@ def main():
     fwd_ms, fwd_n = prof[_lib.KCLASS_FWD_SWEEP]
     bwd_ms, bwd_n = prof[_lib.KCLASS_BWD_SWEEP]
     n_img_local = B * args.steps
-    dv_slots = 592 * 4 if wl.L <= 32 else 592
+    maxlines = max(wl.H, wl.W) * (1 if wl.engine == "trwp" else wl.conn) + (wl.H + wl.W if wl.conn > 4 else 0)
+    dv_slots = 592 * 4 if wl.L <= 32 else min(maxlines, 2048)
     f_tot, f_sw, b_tot, b_sw, f_nl, b_nl = implemented_bytes(wl, E_r, dv_slots)
     # sweeps launched per step (ProfScope brackets one sweep, all its strategy kernels)
     f_launch_ms = fwd_ms / max(fwd_n, 1)

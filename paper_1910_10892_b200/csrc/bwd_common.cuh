@@ -50,7 +50,14 @@ namespace mrf {
 // by __syncwarp().
 constexpr int kDvSlotsSplit = 592;      // persistent CTAs per image of bwd_split (<= 4 per SM)
 constexpr int kDvSlotsSmall = 592 * 4;  // warps per image of bwd_small
-__host__ __device__ inline int dv_slots_for(int L) { return L <= 32 ? kDvSlotsSmall : kDvSlotsSplit; }
+constexpr int kDvSlotsWarp = 2048;      // warps per image of bwd_warp (one line each up to this many)
+// slots one backward call needs for the largest launch of `maxlines` lines
+__host__ __device__ inline int dv_slots_for(int L, int maxlines) {
+  const int m = maxlines > 1 ? maxlines : 1;
+  if (L <= 32) return kDvSlotsSmall;
+  const int w = m < kDvSlotsWarp ? m : kDvSlotsWarp;
+  return w > kDvSlotsSplit ? w : (m < kDvSlotsSplit ? m : kDvSlotsSplit);
+}
 
 struct AccArgs {
   Geometry g;

@@ -5,6 +5,7 @@
 #include "bwd_common.cuh"
 #include "bwd_small.cuh"
 #include "bwd_split.cuh"
+#include "bwd_warp.cuh"
 #include "launch.hpp"
 
 namespace mrf {
@@ -33,11 +34,37 @@ static cudaError_t run_split1(const AccArgs& a, int batch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// banded D <= 2: one warp per line (bwd_warp.cuh)
+template <int EPL, bool TRWP, int RT, bool FULL>
+static cudaError_t run_warp(const AccArgs& a, int batch, cudaStream_t s) {
+  const int wpc = 4;
+  const int smem = bwarp_warp_floats(EPL, acc_rows(TRWP, a.g.R)) * wpc * int(sizeof(float));
+  auto kern = bwd_warp_kernel<EPL, TRWP, RT, FULL>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int warps = a.nlines < kDvSlotsWarp ? a.nlines : kDvSlotsWarp;
+  kern<<<dim3((warps + wpc - 1) / wpc, batch), 32 * wpc, smem, s>>>(a); note_launch();
+  return cudaGetLastError();
+}
+
+// Banded D <= 2 launches with many lines take one warp per line; few lines
+// (C2's 375-row horizontal TRWP sweeps: 2.5 lines per SM) keep the
+// warp-specialised split kernel, whose roles pipeline a lone line's node
+// steps (measured per launch, C2: 375 lines 2.05 ms one-warp vs 0.85 ms
+// split; 1242 lines 0.77 vs 0.77; C3's 7496-line ISGMR launch 3.16 vs
+// 3.61 ms per iteration; C1 0.31 vs 0.32). A/B: MRF_BWD_BAND=split|warp.
+inline bool bwd_band_split(int nlines, int batch) {
+  const char* env = getenv("MRF_BWD_BAND");
+  if (env && (env[0] == 's' || env[0] == 'w')) return env[0] == 's';
+  return int64_t(nlines) * batch < 148 * 9;
+}
+
 // The pairwise strategy is known on the device only: every mode is launched
 // and the instantiations that do not own the sweep exit at once.
 template <int EPL, bool TRWP, int RT, bool FULL>
 static cudaError_t run_split(const AccArgs& a, int batch, cudaStream_t s) {
-  cudaError_t e = run_split1<EPL, TRWP, RT, FULL, 1>(a, batch, s);
+  cudaError_t e = bwd_band_split(a.nlines, batch) ? run_split1<EPL, TRWP, RT, FULL, 1>(a, batch, s)
+                                                  : run_warp<EPL, TRWP, RT, FULL>(a, batch, s);
   if (e == cudaSuccess) e = run_split1<EPL, TRWP, RT, FULL, 2>(a, batch, s);
   if (e == cudaSuccess) e = run_split1<EPL, TRWP, RT, FULL, 0>(a, batch, s);
   return e;

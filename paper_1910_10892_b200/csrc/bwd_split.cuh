@@ -45,8 +45,14 @@
 
 namespace mrf {
 
-constexpr int kSplitSlots = 4;   // node slots between the roles
-constexpr int kPreStages = 3;    // cp.async stages per PRE warp
+#ifndef MRF_SPLIT_SLOTS
+#define MRF_SPLIT_SLOTS 4
+#endif
+#ifndef MRF_PRE_STAGES
+#define MRF_PRE_STAGES 3
+#endif
+constexpr int kSplitSlots = MRF_SPLIT_SLOTS;  // node slots between the roles (A/B: -DMRF_SPLIT_SLOTS=n)
+constexpr int kPreStages = MRF_PRE_STAGES;    // cp.async stages per PRE warp (A/B: -DMRF_PRE_STAGES=n)
 #ifndef MRF_SPLIT_PRE
 #define MRF_SPLIT_PRE 3
 #endif
@@ -210,7 +216,10 @@ __host__ __device__ inline int split_mode(int banded, int D, int L) {
 template <int EPL, bool TRWP, int RT, bool FULL, int NPRE, int MODE>
 // 3 CTAs per SM: few long scanlines (KITTI rows: 375 lines) run in one wave,
 // many lines get 15 warps per SM to hide latency (measured on C2 and C3)
-__global__ void __launch_bounds__(32 * (2 + NPRE), 3) bwd_split_kernel(AccArgs a) {
+#ifndef MRF_SPLIT_MINB
+#define MRF_SPLIT_MINB 3
+#endif
+__global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_kernel(AccArgs a) {
   const bool band = a.desc->banded != 0;
   const int Dband = a.desc->D;
   if (split_mode(band, Dband, a.g.L) != MODE) return;  // another instantiation owns this sweep

@@ -367,8 +367,22 @@ void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap,
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-size_t gvacc_bytes(const mrf_problem_f32* pr) {
-  return sizeof(float) * size_t(pr->batch) * dv_slots_for(pr->labels) * pr->labels * pr->labels;
+// the most lines one backward launch sweeps: TRWP one direction, ISGMR all
+int bwd_max_lines(mrf_topology_t topo, bool trwp) {
+  size_t m = topo->every_line.size();
+  if (trwp) {
+    m = 0;
+    for (const auto& v : topo->dir_lines_all) m = std::max(m, v.size());
+  }
+  return int(m);
+}
+
+int dv_slots(mrf_topology_t topo, const mrf_problem_f32* pr, bool trwp) {
+  return dv_slots_for(pr->labels, bwd_max_lines(topo, trwp));
+}
+
+size_t gvacc_bytes(mrf_topology_t topo, const mrf_problem_f32* pr, bool trwp) {
+  return sizeof(float) * size_t(pr->batch) * dv_slots(topo, pr, trwp) * pr->labels * pr->labels;
 }
 
 size_t dwr_bytes(const mrf_problem_f32* pr, int R, int N) { return sizeof(float) * size_t(pr->batch) * R * N; }
@@ -383,7 +397,8 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
                   const float* grad_cost, const mrf_grads_f32* grads, void* ws, size_t ws_bytes,
                   cudaStream_t stream) {
   const int R = topo->host.num_dirs(), N = topo->host.nodes(), L = pr->labels, B = pr->batch;
-  const size_t mb = messages_bytes(topo, pr), vb = gvacc_bytes(pr);
+  const size_t mb = messages_bytes(topo, pr), vb = gvacc_bytes(topo, pr, TRWP);
+  const int nslots = dv_slots(topo, pr, TRWP);
   const bool isgmr_dw = !TRWP && grads->weight_planes;
   const size_t need = align_up(mb) * (TRWP ? 1 : 2) + align_up(vb) + (TRWP ? 0 : align_up(dwr_bytes(pr, R, N)));
   if (ws_bytes < need || (!ws && need)) fail(MRF_EINVAL, "backward workspace too small");
@@ -423,7 +438,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       const bool fuse = !bwd_uses_small(L, int(topo->dir_lines_all[0].size()), B);
       for (int r = R - 1; r >= 0; --r) {  // directions in reverse (autodiff.hpp:147)
         AccArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), p, q, k, grad_cost,
-                  ain, aout, grads->weight_planes, gvacc, dv_slots_for(L), desc.get(),
+                  ain, aout, grads->weight_planes, gvacc, nslots, desc.get(),
                   (r == 0 && fuse) ? grads->unary : nullptr, dt_src};
         ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         cuda_check(launch_bwd_trwp(a, B, stream), "bwd_split_kernel launch");
@@ -439,7 +454,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
     } else {
       {
         AccArgs a{g, pot, lines + topo->every_start, int(topo->every_line.size()), p, q, k, grad_cost,
-                  ain, aout, isgmr_dw ? dwr : nullptr, gvacc, dv_slots_for(L), desc.get(), nullptr, nullptr};
+                  ain, aout, isgmr_dw ? dwr : nullptr, gvacc, nslots, desc.get(), nullptr, nullptr};
         ProfScope ps(stream, MRF_KCLASS_BWD_SWEEP);
         cuda_check(launch_bwd_isgmr(a, B, stream), "bwd_split_kernel launch");
       }
@@ -460,8 +475,8 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
   if (grads->pairwise) {
     const int64_t total = int64_t(B) * L * L;
     ProfScope ps(stream, MRF_KCLASS_AUX);
-    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, dv_slots_for(L), dv_slots_for(L),
-                                                                           gvacc, grads->pairwise); note_launch();
+    reduce_gvacc_kernel<<<unsigned((total + 255) / 256), 256, 0, stream>>>(B, L, nslots, nslots, gvacc,
+                                                                           grads->pairwise); note_launch();
     cuda_check(cudaGetLastError(), "reduce_gvacc launch");
   }
 }
@@ -616,8 +631,9 @@ size_t mrf_backward_workspace_bytes(mrf_topology_t topo, const mrf_problem_f32* 
   if (!topo || !prob) return 0;
   const size_t mb = align_up(messages_bytes(topo, prob));
   if (engine == MRF_ENGINE_ISGMR)
-    return mb * 2 + align_up(gvacc_bytes(prob)) + align_up(dwr_bytes(prob, topo->host.num_dirs(), topo->host.nodes()));
-  return mb + align_up(gvacc_bytes(prob));
+    return mb * 2 + align_up(gvacc_bytes(topo, prob, false)) +
+           align_up(dwr_bytes(prob, topo->host.num_dirs(), topo->host.nodes()));
+  return mb + align_up(gvacc_bytes(topo, prob, true));
 }
 
 int mrf_isgmr_backward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int iterations, const uint8_t* p,

@@ -335,3 +335,27 @@ def test_non_finite_unary_rejected_at_the_c_abi(engine):
         fwd(mrf, 1)
         torch.cuda.synchronize()
 
+
+
+@pytest.mark.parametrize("mode", ["split", "warp"])
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", [(9, 14, 192, 4, 3, False), (8, 11, 128, 8, 2, True), (10, 13, 16, 4, 3, False),
+                                  (7, 9, 100, 4, 2, True), (1, 20, 64, 4, 2, False)],
+                         ids=["L192c4", "L128c8", "L16c4", "L100c4", "1x20L64"])
+def test_banded_backward_both_kernels(case, engine, mode, monkeypatch):
+    """Banded D <= 2 backward through both kernels (the launcher picks one
+    warp per line for launches with many lines, the warp-specialised split
+    kernel otherwise; forced here), against the reference restatement."""
+    monkeypatch.setenv("MRF_BWD_BAND", mode)
+    H, W, L, conn, K, per_edge = case
+    un, V, wc, planes = WL.random_problem(H, W, L, conn, seed=L * 3 + H, per_edge=per_edge, explicit=False)
+    pr = O.Problem(H, W, L, conn, un, V, wc, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    mrf = to_mrf(pr)
+    f = gpu_forward(engine, mrf, K)
+    assert_forward_equal(f, ref)
+    _, _, gc = O.soft_head(ref.cost, np.random.default_rng(L).uniform(0.25, L - 1.25, H * W), L)
+    g = gpu_backward(engine, mrf, f, gc)
+    assert_grads_close(g, O.backward(engine, pr, K, ref.p, ref.q, gc))
+    g2 = gpu_backward(engine, mrf, f, gc)
+    assert torch.equal(g.pairwise, g2.pairwise) and torch.equal(g.unary, g2.unary)
