@@ -54,7 +54,17 @@ cudaError_t launch_sgm_standard(const Geometry& g, const Potentials& pot, const 
                                 int batch, cudaStream_t s);
 
 // backward kernel choice: one warp per line (L <= 32, many lines) or warp-specialised
-inline bool bwd_uses_small(int L, int nlines, int batch) { return L <= 32 && int64_t(nlines) * batch >= 148 * 16; }
+inline bool bwd_uses_small(int L, int nlines, int batch) {
+  const char* env = getenv("MRF_BWD_SMALL");  // A/B and tests: 0 = never, 1 = whenever L <= 32
+  if (env && (env[0] == '0' || env[0] == '1')) return L <= 32 && env[0] == '1';
+  return L <= 32 && int64_t(nlines) * batch >= 148 * 16;
+}
+// TRWP with the one-warp-per-line small-L kernel: fuse the unary-gradient
+// collection into its direction-0 sweep (else dtheta_acc_kernel per iteration)
+inline bool bwd_small_fuse() {
+  const char* env = getenv("MRF_SMALL_FUSE");
+  return env && env[0] == '1';
+}
 
 // warps per CTA: few long chains -> spread them over every SM
 inline int warps_per_cta(int nlines) {
