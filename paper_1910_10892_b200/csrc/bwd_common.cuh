@@ -108,30 +108,41 @@ __global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__
     const int wn = (d & 1) ? n + g.node_step[d] : n;
     return __ldg(rho_planes + (size_t(b) * (R / 2) + (d >> 1)) * N + min(max(wn, 0), N - 1));
   };
-  if ((L & 3) == 0) {
+  // rho per element only with rho planes (a 4-vector may straddle nodes when L % 4 != 0)
+  const bool per_elem = TRWP && rho_planes != nullptr;
+  if ((NL & 3) == 0) {  // every image's block is 16-byte aligned
     const int n4 = NL >> 2;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-      const int n = (i << 2) / L;
-      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int d = 0; d < R; ++d) {
-        float4 v = __ldcs(reinterpret_cast<const float4*>(Ab + size_t(d) * NL) + i);
-        if (TRWP) {
-          const float rd = rho_of(d, n);
-          v.x = fmul(rd, v.x), v.y = fmul(rd, v.y), v.z = fmul(rd, v.z), v.w = fmul(rd, v.w);
-        }
-        s.x = fadd(s.x, v.x), s.y = fadd(s.y, v.y), s.z = fadd(s.z, v.z), s.w = fadd(s.w, v.w);
-      }
+      float4 v[16];  // R <= 16: every row load in flight before the sums
+#pragma unroll
+      for (int d = 0; d < 16; ++d)
+        if (d < R) v[d] = __ldcs(reinterpret_cast<const float4*>(Ab + size_t(d) * NL) + i);
       float4 o = reinterpret_cast<const float4*>(ds)[i];
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int d = 0; d < 16; ++d) {
+        if (d >= R) continue;
+        float4 t = v[d];
+        if (TRWP) {
+          if (per_elem) {
+            const int e0 = i << 2;
+            t.x = fmul(rho_of(d, e0 / L), t.x), t.y = fmul(rho_of(d, (e0 + 1) / L), t.y);
+            t.z = fmul(rho_of(d, (e0 + 2) / L), t.z), t.w = fmul(rho_of(d, (e0 + 3) / L), t.w);
+          } else {
+            t.x = fmul(rho, t.x), t.y = fmul(rho, t.y), t.z = fmul(rho, t.z), t.w = fmul(rho, t.w);
+          }
+        }
+        s.x = fadd(s.x, t.x), s.y = fadd(s.y, t.y), s.z = fadd(s.z, t.z), s.w = fadd(s.w, t.w);
+      }
       o.x = fadd(o.x, s.x), o.y = fadd(o.y, s.y), o.z = fadd(o.z, s.z), o.w = fadd(o.w, s.w);
       reinterpret_cast<float4*>(dt)[i] = o;
     }
   } else {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < NL; i += gridDim.x * blockDim.x) {
-      const int n = i / L;
       float s = 0.0f;
       for (int d = 0; d < R; ++d) {
         const float v = __ldcs(Ab + size_t(d) * NL + i);
-        s = fadd(s, TRWP ? fmul(rho_of(d, n), v) : v);
+        s = fadd(s, TRWP ? fmul(per_elem ? rho_of(d, i / L) : rho, v) : v);
       }
       dt[i] = fadd(ds[i], s);
     }

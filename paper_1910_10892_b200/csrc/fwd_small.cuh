@@ -14,8 +14,26 @@
 
 namespace mrf {
 
-// per-warp ring stage: ROWS rows of 32 floats + {w, rho}
-__host__ __device__ constexpr int fwd_small_stage(int rows) { return rows * 32 + 2; }
+// per-warp ring stage: ROWS rows of 32 floats + {w, rho}, padded to 16 B
+__host__ __device__ constexpr int fwd_small_stage(int rows) { return rows * 32 + 4; }
+// per-warp floats: the ring + base(mu) of the current node (32, 16 B aligned)
+__host__ __device__ constexpr int fwd_small_warp_floats(int rows, int stages) { return stages * fwd_small_stage(rows) + 32; }
+
+__device__ __forceinline__ uint64_t pack2f(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void unpack2f(uint64_t v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+// two IEEE round-to-nearest adds in one FADD2 (products stay scalar: ptxas
+// would contract mul.rn.f32x2 + add.rn.f32x2 into FFMA2)
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 template <bool TRWP, int R, int LMAX, bool WPL>
 __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
@@ -27,7 +45,8 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
   const Geometry& g = a.g;
   const int L = g.L, N = g.N;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  float* ring = smem + size_t(wid) * kStages * STG;
+  float* ring = smem + size_t(wid) * fwd_small_warp_floats(ROWS, kStages);
+  float* s_base = ring + kStages * STG;  // base(mu) of the current node, broadcast to every label
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   const int b = blockIdx.y;
   const bool valid = lane < L;
@@ -108,20 +127,34 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
       // ---- dense min-plus, ascending mu, strict '<': independent chains over
       // mu blocks of 8 (shorter dependency chains), merged in index order with
-      // the earlier block winning ties
+      // the earlier block winning ties. base(mu) comes from a 16-byte
+      // broadcast load of the staged row (4 mu per load), two candidates
+      // share one packed add.
       constexpr int NB = LMAX / 8;
       float bb[NB];
       int ba[NB];
 #pragma unroll
       for (int c = 0; c < NB; ++c) bb[c] = kInf, ba[c] = 0;
+      s_base[lane] = base;
+      __syncwarp();
 #pragma unroll
-      for (int mu = 0; mu < LMAX; ++mu) {
-        const float bm = __shfl_sync(0xffffffffu, base, mu);
-        const int c = mu / 8;
-        const float v = fadd(bm, wpl ? fmul(w, vcol[mu]) : wv[mu]);
-        const bool p = v < bb[c];
-        bb[c] = p ? v : bb[c];
-        ba[c] = p ? mu : ba[c];
+      for (int m4 = 0; m4 < LMAX; m4 += 4) {
+        const ulonglong2 b4 = *reinterpret_cast<const ulonglong2*>(s_base + m4);
+        float v[4];
+        if (wpl) {
+          unpack2f(fadd2(b4.x, pack2f(fmul(w, vcol[m4]), fmul(w, vcol[m4 + 1]))), v[0], v[1]);
+          unpack2f(fadd2(b4.y, pack2f(fmul(w, vcol[m4 + 2]), fmul(w, vcol[m4 + 3]))), v[2], v[3]);
+        } else {
+          unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[0], v[1]);
+          unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[2], v[3]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int mu = m4 + u, c = mu / 8;
+          const bool p = v[u] < bb[c];
+          bb[c] = p ? v[u] : bb[c];
+          ba[c] = p ? mu : ba[c];
+        }
       }
       float best = bb[0];
       int arg = ba[0];
