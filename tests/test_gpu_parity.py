@@ -361,14 +361,14 @@ def test_banded_backward_both_kernels(case, engine, mode, monkeypatch):
     assert torch.equal(g.pairwise, g2.pairwise) and torch.equal(g.unary, g2.unary)
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
+@pytest.mark.parametrize("kernel", [("0",), ("1",)], ids=["small", "small_fused"])
 @pytest.mark.parametrize("engine", ["isgmr", "trwp"])
-def test_small_label_backward_many_lines(engine, fuse, monkeypatch):
+def test_small_label_backward_many_lines(engine, kernel, monkeypatch):
     """The one-warp-per-line small-L backward (bwd_small.cuh: C4's kernel,
     picked for L <= 32 with >= 2368 lines per launch): 30 images of 80 x 80,
     explicit 21 x 21 V, per-edge weights, each image against the reference
     restatement; with and without the fused unary-gradient sweep."""
-    monkeypatch.setenv("MRF_SMALL_FUSE", fuse)
+    monkeypatch.setenv("MRF_SMALL_FUSE", kernel[0])
     H, W, L, conn, K, B = 80, 80, 21, 4, 2, 30
     wl = WL.seg_batch(H, W, L, B, K=K, first=3)
     prs = [O.Problem(H, W, L, conn, wl.unary[b], wl.V, 1.0, wl.w_planes[b], 0.5, None) for b in range(B)]
