@@ -11,6 +11,10 @@
 
 #include "fwd_warp.cuh"
 
+#ifndef MRF_BAND2_COOP
+#define MRF_BAND2_COOP 1
+#endif
+
 namespace mrf {
 
 __host__ __device__ constexpr int band2_smem_floats(int EPL, int rows, int stages = kStages) {
@@ -107,6 +111,8 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
     // (C2 +2 %: the lone-warp horizontal sweeps are scheduling-sensitive), so
     // those recompute the addresses.
     constexpr bool kIncIssue = EPL <= 2;
+    // FULL rows at 6 labels per lane: whole-row 16-byte chunks (MRF_BAND2_COOP=0: per-lane slices)
+    constexpr bool kCoopIssue = FULL && EPL == 6 && MRF_BAND2_COOP;
     const ptrdiff_t row_step = ptrdiff_t(st) * L;
     if (kIncIssue) {
 #pragma unroll
@@ -130,7 +136,17 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
         const int slot = (j - 1) % ST;
         const int prev = ld.first + (j - 1) * st;
         const size_t off = size_t(prev) * L;
-        if (FULL || nvalid > 0) {
+        if (kCoopIssue) {
+          // 16-byte chunks of the whole row, lanes = chunks (a lane's own 24-byte
+          // slice would take three 8-byte copies); readers sync the warp
+#pragma unroll
+          for (int rr = 0; rr < ROWS; ++rr) {
+            const float* src = rowp[rr] - l0 + off;
+#pragma unroll
+            for (int u = lane; u < 8 * EPL; u += 32)
+              cp_async_u32(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + 4 * u), src + 4 * u, 16);
+          }
+        } else if (FULL || nvalid > 0) {
 #pragma unroll
           for (int rr = 0; rr < ROWS; ++rr)
             cp_slice_t<EPL, FULL>(ring_s + 4u * uint32_t((slot * ROWS + rr) * LS + l0), rowp[rr] + off, nvalid);
@@ -156,6 +172,7 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       if (j + ST - 1 <= nsteps) issue(j + ST - 1);
       cp_commit();
       cp_wait<ST - 1>();
+      if (kCoopIssue) __syncwarp();  // rows were copied by other lanes
       const int slot = kIncIssue ? slot_c : (j - 1) % ST;  // ring slot of node step j
       slot_c = slot_c == ST - 1 ? 0 : slot_c + 1;
       const float* srow = ring + slot * ROWS * LS + l0;
