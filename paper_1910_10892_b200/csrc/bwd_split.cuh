@@ -503,12 +503,12 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
           near[i] = valid && uint32_t(d + (WIN ? kWin : 1)) <= uint32_t(WIN ? 2 * kWin : 2);
           far[i] = valid && !near[i];
           // targets l-1 / l / l+1 go through registers in every mode (the
-          // window masks carry only 2 <= |d| <= kWin)
-          mword |= (valid && d == -1 ? 1u : 0u) << i;
-          mword |= (valid && d == 0 ? 1u : 0u) << (8 + i);
-          mword |= (valid && d == 1 ? 1u : 0u) << (16 + i);
-          kmn = far[i] ? min(kmn, mu[i]) : kmn;
-          kmx = far[i] ? max(kmx, mu[i]) : kmx;
+          // window masks carry only 2 <= |d| <= kWin): code c = d + 1 in
+          // {0, 1, 2} sets bit 8c + i
+          const uint32_t c = uint32_t(d + 1);
+          mword |= (valid && c <= 2u) ? (1u << (8 * c + i)) : 0u;
+          kmn = min(kmn, far[i] ? mu[i] : 0x7fffffff);
+          kmx = max(kmx, far[i] ? mu[i] : -1);
         }
         const float S = warp_sum_f(lsum);
         kmn = __reduce_min_sync(0xffffffffu, kmn);
