@@ -68,6 +68,18 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// shared-window addresses of the barriers, computed once per kernel
+__device__ __forceinline__ void mbar_arrive(uint32_t bar_s) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar_s) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar_s, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar_s),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -252,9 +264,9 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_red + 32);  // full[NS], done[NS], empty[NS]
   float* s_c = reinterpret_cast<float*>(bars + 3 * kSplitSlots + 4);  // WIN: chain carry row (padded)
   float* s_dv = s_c + 32 * (EPL + 1);                                    // WIN: [32*EPL][2*kWin+1]
-  uint64_t* bar_full = bars;
-  uint64_t* bar_done = bars + kSplitSlots;
-  uint64_t* bar_empty = bars + 2 * kSplitSlots;
+  const uint32_t bar_full = smem_u32(bars);  // [slot] at + 8 * slot
+  const uint32_t bar_done = bar_full + 8u * kSplitSlots;
+  const uint32_t bar_empty = bar_full + 16u * kSplitSlots;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 3 * kSplitSlots; ++i) mbar_init(bars + i, 32);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -566,7 +578,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
         const int slot = int(gs % kSplitSlots);
         const uint32_t use = gs / kSplitSlots;
         PMARK(2);
-        if (use > 0) SPLIT_WAIT(bar_empty + slot, (use - 1) & 1u);
+        if (use > 0) SPLIT_WAIT(bar_empty + 8u * slot, (use - 1) & 1u);
         PMARK(3);
         float* sl = slots + slot * SLOT;
         uint16_t* olist = reinterpret_cast<uint16_t*>(sl + SL::OTH);
@@ -631,7 +643,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
           sc[SC_W] = __float_as_uint(wpl ? xs[1] : a.pot.w);
           sc[SC_RHO] = __float_as_uint(TRWP ? (rpl ? xs[2] : a.pot.rho) : 1.0f);
         }
-        mbar_arrive(bar_full + slot);
+        mbar_arrive(bar_full + 8u * slot);
         PMARK(5);
       }
       cp_wait<0>();
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
       for (int s = 0; s < nsteps; ++s) {
         const uint32_t gs = gs0 + uint32_t(s);
         const int slot = int(gs % kSplitSlots);
-        SPLIT_WAIT(bar_full + slot, (gs / kSplitSlots) & 1u);
+        SPLIT_WAIT(bar_full + 8u * slot, (gs / kSplitSlots) & 1u);
         float* sl = slots + slot * SLOT;
         const uint32_t* sc = reinterpret_cast<const uint32_t*>(sl + SL::SC);
         const int main_t = int(sc[SC_MAIN]);
@@ -667,7 +679,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
                                lane);
         sts_slice<EPL>(sl + SL::CIN + l0, carry);
         sts_slice<EPL>(sl + SL::ACC + l0, acc);
-        mbar_arrive(bar_done + slot);
+        mbar_arrive(bar_done + 8u * slot);
 #pragma unroll
         for (int i = 0; i < EPL; ++i) carry[i] = TRWP ? fmul(rho, acc[i]) : acc[i];
       }
@@ -723,7 +735,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
       for (int s = 0; s < nsteps; ++s) {
         const uint32_t gs = gs0 + uint32_t(s);
         const int slot = int(gs % kSplitSlots);
-        SPLIT_WAIT(bar_done + slot, (gs / kSplitSlots) & 1u);
+        SPLIT_WAIT(bar_done + 8u * slot, (gs / kSplitSlots) & 1u);
         const float* sl = slots + slot * SLOT;
         const uint32_t* sc = reinterpret_cast<const uint32_t*>(sl + SL::SC);
         const int qv = int(sc[SC_Q]);
@@ -816,7 +828,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
           }
         }
         __syncwarp();
-        mbar_arrive(bar_empty + slot);
+        mbar_arrive(bar_empty + 8u * slot);
       }
       if (fuse) {
         // the head is no edge's cur: dtheta(head) += sum_{d != 0} rho_d A[d](head) + rho acc_last
