@@ -789,17 +789,33 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
           if (do_w) wpart = fadd(fmul(fsub(gb0, gbD), s0), fmul(fsub(gb1, gbD), s1));
         } else {
           const uint8_t* pb = reinterpret_cast<const uint8_t*>(sl + SL::P);
+          // V'(p_l, l) of every label first: independent loads in flight
+          // together instead of one L1 round trip per label in the dw chain
+          float vvs[EPL];
+          int ms[EPL];
+#pragma unroll
+          for (int i = 0; i < EPL; ++i) {
+            const int l = l0 + i;
+            const bool valid = FULL || i < nvalid;
+            ms[i] = valid ? int(pb[l]) : l;
+            const int d = ms[i] - l;
+            vvs[i] = !do_w ? 0.0f : band ? __ldg(gband + min(abs(d), Dband)) : __ldg(a.pot.V + ms[i] * vs_mu + l * vs_l);
+          }
 #pragma unroll
           for (int i = 0; i < EPL; ++i) {
             const float ga = wpl ? fmul(gg[i], w) : gg[i];
             const bool cf = bit(mword, 24 + i);
             const int l = l0 + i;
             const bool valid = FULL || i < nvalid;
-            const int m = valid ? int(pb[l]) : l;
+            const int m = ms[i];
             const int d = m - l;
             if (WIN) {
-              // near-band dV partial of (m, l): shared accumulator, one owner lane per label
-              if (valid && d >= -kWin && d <= kWin && ga != 0.0f) atomicAdd(s_dv + l * (2 * kWin + 1) + d + kWin, ga);
+              // near-band dV partial of (m, l): this lane owns row l of the
+              // shared accumulator, so a plain read-modify-write suffices
+              if (valid && d >= -kWin && d <= kWin && ga != 0.0f) {
+                float* dv = s_dv + l * (2 * kWin + 1) + d + kWin;
+                *dv = fadd(*dv, ga);
+              }
             } else {
               const bool cm = bit(mword, i), c0 = bit(mword, 8 + i), cp = bit(mword, 16 + i);
               vacc[i][0] = fadd(vacc[i][0], cm ? ga : 0.0f);
@@ -808,8 +824,7 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
             }
             fval[i] = fadd(fval[i], cf ? ga : 0.0f);
             if (do_w && valid && gg[i] != 0.0f) {
-              const float vv = band ? __ldg(gband + min(abs(d), Dband)) : __ldg(a.pot.V + m * vs_mu + l * vs_l);
-              wpart = fadd(wpart, fmul(gg[i], vv));
+              wpart = fadd(wpart, fmul(gg[i], vvs[i]));
             }
           }
         }
