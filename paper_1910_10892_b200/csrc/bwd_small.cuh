@@ -115,24 +115,33 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
 #pragma unroll
     for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] = sd[rr] < 0 ? dcb : ainb + size_t(sd[rr] > 0 ? sd[rr] : 0) * NL;
 
-    auto issue = [&](int s) {
-      const uint32_t base_s = ring_s + 4u * uint32_t((s % kStages) * stage_f);
-      const int j = nsteps - s;
-      const int ocur = o_first + j * stL;
+    // incremental issue state: row pointers at node cur, ring slot, edge
+    // (index and p byte offset), all stepped back one node per issue
+#pragma unroll
+    for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] += o_first + nsteps * stL;
+    int islot = 0, cur_i = ld.first + nsteps * st;
+    uint32_t e_i = ebase + uint32_t(nsteps - 1);
+    size_t pb_i = size_t(e_i) * L;
+    auto issue = [&](int /*s*/) {
+      const uint32_t base_s = ring_s + 4u * uint32_t(islot * stage_f);
       if (valid) {
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr)
           if (rr < nrows)
-            cp_async_u32(base_s + 4u * (rr * 32 + lane), rowb[rr] + ocur, 4);
+            cp_async_u32(base_s + 4u * (rr * 32 + lane), rowb[rr], 4);
       }
-      const uint32_t e = ebase + uint32_t(j - 1);
-      const size_t pb = size_t(e) * L;
+#pragma unroll
+      for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] -= stL;
+      const uint32_t e = e_i;
+      const size_t pb = pb_i;
+      const int cur = cur_i;
+      --e_i, pb_i -= L, cur_i -= st;
+      islot = islot == kStages - 1 ? 0 : islot + 1;
       const uint32_t* pw = reinterpret_cast<const uint32_t*>(pimg) + (pb >> 2);
       const int nwords = int(((pb + L - 1) >> 2) - (pb >> 2)) + 1;
       const uint32_t pdst = base_s + 4u * (NR * 32);
       if (lane < nwords) cp_async_u32(pdst + 4u * lane, pw + lane, 4);
       const uint32_t xdst = pdst + 4u * 12;
-      const int cur = ld.first + j * st;
       const int wnode = (r & 1) ? cur : cur - st;
       if (lane == 0) cp_async_u32(xdst, reinterpret_cast<const uint32_t*>(qimg) + (e >> 2), 4);
       if (wpl && lane == 1) cp_async_u32(xdst + 4u, wrow + wnode, 4);
@@ -158,12 +167,15 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
     // fused unary gradient: dtheta(cur) loaded one step ahead
     float dtn = (fuse && valid && nsteps > 0) ? __ldcg(dths + o_first + nsteps * stL + lane) : 0.0f;
 
+    int cslot = 0;
+    float* aout_p = aoutb + size_t(r) * NL + o_first + (nsteps - 1) * stL;  // A row of step 0's prev
     for (int s = 0; s < nsteps; ++s) {
       if (s + kStages - 1 < nsteps) issue(s + kStages - 1);
       cp_commit();
       cp_wait<kStages - 1>();
       __syncwarp();  // p / q words were copied by other lanes
-      const float* stg = ring + (s % kStages) * stage_f;
+      const float* stg = ring + cslot * stage_f;
+      cslot = cslot == kStages - 1 ? 0 : cslot + 1;
       const int j = nsteps - s;
       const uint32_t e = ebase + uint32_t(j - 1);
       const uint8_t* prow = reinterpret_cast<const uint8_t*>(stg + NR * 32) + ((size_t(e) * L) & 3);
@@ -226,7 +238,8 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
         m &= m - 1;
         if (k >= 0) acc = fadd(acc, s_g[k]);
       }
-      if (valid) aoutb[size_t(r) * NL + o_first + (j - 1) * stL] = acc;
+      if (valid) *aout_p = acc;
+      aout_p -= stL;
       // fused unary gradient: dtheta(cur) += sum_d rho_d A[d](cur) + this sweep's share
       if (fuse && valid) {
         const float dnew = fadd(fadd(dtn, rsum), carry);

@@ -80,16 +80,24 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
     }
     const float* wrow = wpl ? a.pot.w_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
     const float* rrow = rpl ? a.pot.rho_planes + (size_t(b) * (R / 2) + fam) * N : nullptr;
-    auto issue = [&](int j) {
-      const uint32_t base_s = ring_s + 4u * uint32_t(((j - 1) % kStages) * STG);
-      const int prev = ld.first + (j - 1) * st;
+    // incremental issue state (row pointers, ring slot, edge node) advanced
+    // one node step per issue: no 64-bit index arithmetic per step
+    const ptrdiff_t row_step = ptrdiff_t(st) * L;
+#pragma unroll
+    for (int rr = 0; rr < ROWS; ++rr) rowp[rr] += ptrdiff_t(ld.first) * L;
+    int islot = 0, wnode_i = (r & 1) ? ld.first + st : ld.first;
+    auto issue = [&](int /*j*/) {
+      const uint32_t base_s = ring_s + 4u * uint32_t(islot * STG);
       if (valid) {
 #pragma unroll
-        for (int rr = 0; rr < ROWS; ++rr) cp_async_u32(base_s + 4u * (rr * 32 + lane), rowp[rr] + size_t(prev) * L, 4);
+        for (int rr = 0; rr < ROWS; ++rr) cp_async_u32(base_s + 4u * (rr * 32 + lane), rowp[rr], 4);
       }
-      const int wnode = (r & 1) ? prev + st : prev;
-      if (wpl && lane == 0) cp_async_u32(base_s + 4u * (ROWS * 32), wrow + wnode, 4);
-      if (rpl && lane == 1) cp_async_u32(base_s + 4u * (ROWS * 32 + 1), rrow + wnode, 4);
+      if (wpl && lane == 0) cp_async_u32(base_s + 4u * (ROWS * 32), wrow + wnode_i, 4);
+      if (rpl && lane == 1) cp_async_u32(base_s + 4u * (ROWS * 32 + 1), rrow + wnode_i, 4);
+#pragma unroll
+      for (int rr = 0; rr < ROWS; ++rr) rowp[rr] += row_step;
+      wnode_i += st;
+      islot = islot == kStages - 1 ? 0 : islot + 1;
     };
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) {
@@ -97,15 +105,20 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       cp_commit();
     }
     const size_t pq_base = (size_t(b) * g.K_cap + a.k) * g.E + g.dir_offset[r] + ld.edge_base;
-    float* mout = a.m_out + img + size_t(r) * N * L + lane;
+    // output pointers at node step 1, advanced one step per node
+    uint8_t* pout = a.p + pq_base * L + lane;
+    uint8_t* qout = a.q + pq_base;
+    float* mout = a.m_out + img + size_t(r) * N * L + lane + ptrdiff_t(ld.first + st) * L;
     float carry = 0.0f;
+    int cslot = 0;
 
     for (int j = 1; j <= nsteps; ++j) {
       if (j + kStages - 1 <= nsteps) issue(j + kStages - 1);
       cp_commit();
       cp_wait<kStages - 1>();
       __syncwarp();  // the edge scalars were copied by lanes 0 / 1
-      const float* srow = ring + ((j - 1) % kStages) * STG + lane;
+      const float* srow = ring + cslot * STG + lane;
+      cslot = cslot == kStages - 1 ? 0 : cslot + 1;
       // ---- base (isgmr.hpp:82-88 / trwp.hpp:84-90 addition order)
       float base;
       if (!TRWP) {
@@ -165,7 +178,8 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
         arg = p ? ba[c] : arg;
       }
       // ---- p, reparametrisation first argmin (lowest label, -0 as the reference)
-      if (valid) a.p[(pq_base + j - 1) * L + lane] = uint8_t(arg);
+      if (valid) *pout = uint8_t(arg);
+      pout += L;
       const uint32_t lk = valid ? order_key(fadd(best, 0.0f)) : 0xffffffffu;
       const uint32_t lt = valid ? (uint32_t(lane) << 1) | (__float_as_uint(best) == 0x80000000u ? 1u : 0u) : 0xffffffffu;
       const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
@@ -173,9 +187,10 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       float lo = key_value(kmin);
       if (tmin & 1u) lo = -0.0f;
       carry = fsub(best, lo);
-      const int cur = ld.first + j * st;
-      if (valid) mout[size_t(cur) * L] = carry;
-      if (lane == 0) a.q[pq_base + j - 1] = uint8_t(tmin >> 1);
+      if (valid) *mout = carry;
+      mout += row_step;
+      if (lane == 0) *qout = uint8_t(tmin >> 1);
+      ++qout;
     }
     cp_wait<0>();
     __syncwarp();
