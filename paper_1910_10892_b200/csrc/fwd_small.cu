@@ -4,17 +4,24 @@
 
 namespace mrf {
 
-template <bool TRWP, int R, int LMAX, bool WPL>
-static cudaError_t run1(const FwdArgs& a, int batch, cudaStream_t s) {
+template <bool TRWP, int R, int LMAX, bool WPL, bool AGG>
+static cudaError_t run1a(const FwdArgs& a, int batch, cudaStream_t s) {
   constexpr int rows = 1 + (TRWP ? R - 1 : R - 2);
   const int wpc = 4;
   const int smem = fwd_small_warp_floats(rows, kStages) * int(sizeof(float)) * wpc;
-  auto kern = fwd_small_kernel<TRWP, R, LMAX, WPL>;
+  auto kern = fwd_small_kernel<TRWP, R, LMAX, WPL, AGG>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int blocks = (a.nlines + wpc - 1) / wpc < 65535 ? (a.nlines + wpc - 1) / wpc : 65535;
   kern<<<dim3(blocks, batch), 32 * wpc, smem, s>>>(a); note_launch();
   return cudaGetLastError();
+}
+
+template <bool TRWP, int R, int LMAX, bool WPL>
+static cudaError_t run1(const FwdArgs& a, int batch, cudaStream_t s) {
+  // the aggregation rides on TRWP's last 4-direction sweep (host sets agg_*)
+  if (TRWP && R == 4 && (a.agg_cost || a.agg_labels)) return run1a<TRWP, R, LMAX, WPL, TRWP && R == 4>(a, batch, s);
+  return run1a<TRWP, R, LMAX, WPL, false>(a, batch, s);
 }
 
 template <bool TRWP, int R, int LMAX>

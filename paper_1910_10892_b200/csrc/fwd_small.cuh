@@ -35,7 +35,11 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return r;
 }
 
-template <bool TRWP, int R, int LMAX, bool WPL>
+// AGG (TRWP, last sweep only, every node on a line of that direction): the
+// base sum s = theta + sum_d m^d at prev is that node's aggregated cost in
+// the reference's order (inference.hpp:40-57), so the sweep also writes the
+// cost row and the first-argmin label (the tail of each line at its end).
+template <bool TRWP, int R, int LMAX, bool WPL, bool AGG = false>
 __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
   if (a.desc->banded || WPL != (a.pot.w_planes != nullptr)) return;  // another kernel owns the sweep
   extern __shared__ float smem[];
@@ -111,6 +115,15 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
     float* mout = a.m_out + img + size_t(r) * N * L + lane + ptrdiff_t(ld.first + st) * L;
     float carry = 0.0f;
     int cslot = 0;
+    // cost row + first argmin label of node n from its summed row c
+    auto agg_row = [&](int n, float c) {
+      const size_t nb = size_t(b) * N + n;
+      if (a.agg_cost && valid) a.agg_cost[nb * L + lane] = c;
+      const uint32_t kk = valid ? order_key(fadd(c, 0.0f)) : 0xffffffffu;
+      const uint32_t kmin = __reduce_min_sync(0xffffffffu, kk);
+      const uint32_t lmin = __reduce_min_sync(0xffffffffu, kk == kmin ? uint32_t(lane) : 0xffffffffu);
+      if (lane == 0 && a.agg_labels) a.agg_labels[nb] = uint16_t(lmin);
+    };
 
     for (int j = 1; j <= nsteps; ++j) {
       if (j + kStages - 1 <= nsteps) issue(j + kStages - 1);
@@ -135,6 +148,7 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
           s = fadd(s, d == r ? carry : t);
         }
         base = fsub(fmul(rho, s), mo);
+        if (AGG) agg_row(ld.first + (j - 1) * st, s);
       }
       const float w = wpl ? srow[ROWS * 32 - lane] : 0.0f;
       if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
@@ -191,6 +205,15 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       mout += row_step;
       if (lane == 0) *qout = uint8_t(tmin >> 1);
       ++qout;
+    }
+    if (TRWP && AGG) {
+      // the tail is no edge's prev: its cost from its rows and the final message
+      const int tail = ld.first + nsteps * st;
+      float c = valid ? __ldcg(a.pot.unary + (size_t(b) * N + tail) * L + lane) : 0.0f;
+#pragma unroll
+      for (int d = 0; d < R; ++d)
+        c = fadd(c, d == r ? carry : (valid ? __ldcg(a.m_in + img + (size_t(d) * N + tail) * L + lane) : 0.0f));
+      agg_row(tail, c);
     }
     cp_wait<0>();
     __syncwarp();

@@ -336,15 +336,17 @@ void launch_forward_sweep(const mrf_problem_f32* pr, const Geometry& g, const Li
   cuda_check(launch_fwd_generic(a, pr->batch, TRWP, stream), "fwd_warp_kernel launch");
 }
 
+// fused: bit 0 -- the banded D == 2 forward aggregated in its last sweep;
+// bit 1 -- the dense small-L forward did (each only when it owned the call)
 void launch_aggregate(const mrf_problem_f32* pr, int R, int N, const float* messages, float* cost, uint16_t* labels,
-                      cudaStream_t stream, const PairDesc* desc = nullptr, bool fused_by_band2 = false) {
+                      cudaStream_t stream, const PairDesc* desc = nullptr, int fused = 0) {
   if (!cost && !labels) return;
   const int64_t warps = int64_t(pr->batch) * N;
   const int per_block = 8;
-  const int64_t blocks = (warps + per_block - 1) / per_block;
+  const int64_t blocks = std::min<int64_t>((warps + per_block - 1) / per_block, 148 * 16);
   ProfScope ps(stream, MRF_KCLASS_AGGREGATE);
   aggregate_kernel<<<unsigned(blocks), per_block * 32, 0, stream>>>(pr->batch, N, pr->labels, R, pr->unary, messages,
-                                                                    cost, labels, desc, fused_by_band2 ? 1 : 0);
+                                                                    cost, labels, desc, fused);
   note_launch();
   cuda_check(cudaGetLastError(), "aggregate_kernel launch");
 }
@@ -588,8 +590,9 @@ int mrf_trwp_forward_f32(mrf_topology_t topo, const mrf_problem_f32* prob, int i
       trwp_step(topo, prob, k, iterations, out->messages, out->p, out->q, desc.get(), stream,
                 last ? out->cost : nullptr, last ? out->labels : nullptr);
     }
+    const int fused = fuse ? (1 | (fwd_small_applies(prob->labels, topo->host.num_dirs()) ? 2 : 0)) : 0;
     launch_aggregate(prob, topo->host.num_dirs(), topo->host.nodes(), out->messages, out->cost, out->labels, stream,
-                     desc.get(), fuse);
+                     desc.get(), fused);
     finite.finish("trwp_forward");
   });
 }
