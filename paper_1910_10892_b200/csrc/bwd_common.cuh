@@ -92,8 +92,10 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 // ascending: the iteration's contribution of every sweep to the unary
 // gradient (autodiff.hpp:101 / :173). Image b = blockIdx.y; float4 when L % 4
 // == 0 (a vector never straddles two nodes).
-template <bool TRWP>
-__global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__ A, float rho,
+// RT: the direction count as a compile-time bound (4, 8 or 16): the row
+// loads of one vector stay in registers without capping occupancy.
+template <bool TRWP, int RT = 16>
+__global__ void __launch_bounds__(256) dtheta_acc_kernel(int R, int N, int L, const float* __restrict__ A, float rho,
                                   const float* __restrict__ rho_planes, Geometry g, float* __restrict__ dtheta,
                                   const float* dtheta_src) {
   // dtheta = dtheta_src + sum_d rho_d A[d]; dtheta_src is dc on the first update
@@ -113,14 +115,14 @@ __global__ void dtheta_acc_kernel(int R, int N, int L, const float* __restrict__
   if ((NL & 3) == 0) {  // every image's block is 16-byte aligned
     const int n4 = NL >> 2;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
-      float4 v[16];  // R <= 16: every row load in flight before the sums
+      float4 v[RT];  // every row load in flight before the sums
 #pragma unroll
-      for (int d = 0; d < 16; ++d)
+      for (int d = 0; d < RT; ++d)
         if (d < R) v[d] = __ldcs(reinterpret_cast<const float4*>(Ab + size_t(d) * NL) + i);
       float4 o = reinterpret_cast<const float4*>(ds)[i];
       float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int d = 0; d < 16; ++d) {
+      for (int d = 0; d < RT; ++d) {
         if (d >= R) continue;
         float4 t = v[d];
         if (TRWP) {

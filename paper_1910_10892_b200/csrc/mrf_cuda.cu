@@ -369,6 +369,18 @@ void trwp_step(mrf_topology_t topo, const mrf_problem_f32* pr, int k, int K_cap,
 
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
+template <bool TRWP>
+void launch_dtheta_acc(dim3 grid, cudaStream_t s, int R, int N, int L, const float* A, float rho, const float* rho_planes,
+                       const Geometry& g, float* dtheta, const float* src) {
+  if (R <= 4)
+    dtheta_acc_kernel<TRWP, 4><<<grid, 256, 0, s>>>(R, N, L, A, rho, rho_planes, g, dtheta, src);
+  else if (R <= 8)
+    dtheta_acc_kernel<TRWP, 8><<<grid, 256, 0, s>>>(R, N, L, A, rho, rho_planes, g, dtheta, src);
+  else
+    dtheta_acc_kernel<TRWP, 16><<<grid, 256, 0, s>>>(R, N, L, A, rho, rho_planes, g, dtheta, src);
+  note_launch();
+}
+
 // the most lines one backward launch sweeps: TRWP one direction, ISGMR all
 int bwd_max_lines(mrf_topology_t topo, bool trwp) {
   size_t m = topo->every_line.size();
@@ -448,8 +460,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       }
       if (!fuse) {
         ProfScope ps(stream, MRF_KCLASS_AUX);
-        dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary,
-                                                             dt_src); note_launch();
+        launch_dtheta_acc<TRWP>(dt_grid, stream, R, N, L, aout, pr->rho, pr->rho_planes, g, grads->unary, dt_src);
         dt_src = grads->unary;
         cuda_check(cudaGetLastError(), "dtheta_acc launch");
       }
@@ -462,8 +473,7 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       }
       // ISGMR's directions run concurrently: the unary gradient is collected after the launch
       ProfScope ps(stream, MRF_KCLASS_AUX);
-      dtheta_acc_kernel<TRWP><<<dt_grid, 256, 0, stream>>>(R, N, L, aout, pr->rho, nullptr, g, grads->unary, dt_src);
-      note_launch();
+      launch_dtheta_acc<TRWP>(dt_grid, stream, R, N, L, aout, pr->rho, nullptr, g, grads->unary, dt_src);
       dt_src = grads->unary;
       cuda_check(cudaGetLastError(), "dtheta_acc launch");
     }
