@@ -124,10 +124,16 @@ __device__ __forceinline__ void window_gather(float (&acc)[EPL], const uint32_t 
 #pragma unroll
   for (int i = 0; i < EPL; ++i) {
     uint32_t m = wm[i];
+    // two sources per trip: both loads in flight, added in ascending order
     while (m) {
-      const int k = __ffs(m) - 1;
+      const int k1 = __ffs(m) - 1;
       m &= m - 1;
-      acc[i] = fadd(acc[i], val(l0 + i + k - kWin));
+      const int k2 = m ? __ffs(m) - 1 : k1;
+      const bool two = m != 0u;
+      m &= m - 1;
+      const float v1 = val(l0 + i + k1 - kWin), v2 = val(l0 + i + k2 - kWin);
+      acc[i] = fadd(acc[i], v1);
+      if (two) acc[i] = fadd(acc[i], v2);
     }
   }
 }
