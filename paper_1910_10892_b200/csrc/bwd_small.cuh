@@ -233,10 +233,15 @@ __global__ void __launch_bounds__(128) bwd_small_kernel(AccArgs a) {
       uint32_t m = s_m[lane];
       const int nit = int(__reduce_max_sync(0xffffffffu, uint32_t(__popc(m))));
       float acc = lane == main_mu ? F : 0.0f;
-      for (int it = 0; it < nit; ++it) {
-        const int k = __ffs(m) - 1;
+      // two sources per trip (ascending): both loads in flight
+      for (int it = 0; it < nit; it += 2) {
+        const int k1 = __ffs(m) - 1;
         m &= m - 1;
-        if (k >= 0) acc = fadd(acc, s_g[k]);
+        const int k2 = __ffs(m) - 1;
+        m &= m - 1;
+        const float v1 = s_g[k1 >= 0 ? k1 : 0], v2 = s_g[k2 >= 0 ? k2 : 0];
+        if (k1 >= 0) acc = fadd(acc, v1);
+        if (k2 >= 0) acc = fadd(acc, v2);
       }
       if (valid) *aout_p = acc;
       aout_p -= stL;
