@@ -306,7 +306,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
     ap.add_argument("--engine", default=None, choices=[None, "isgmr", "trwp"], help="C5's engine (default ISGMR)")
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    # enough steps that the pipeline's fill (the first H2D) and drain (the last
+    # D2H) do not dominate the end-to-end rate
+    ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
