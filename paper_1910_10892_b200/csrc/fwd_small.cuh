@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
 #pragma unroll
       for (int mu = 0; mu < LMAX; ++mu) wv[mu] = wpl ? 0.0f : fmul(a.pot.w, vcol[mu]);
     }
+    float w_last = __uint_as_float(0xffffffffu);  // per-edge w of the cached products: none yet
     const float* rowp[ROWS];
     rowp[0] = un;
 #pragma unroll
@@ -151,6 +152,14 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
         if (AGG) agg_row(ld.first + (j - 1) * st, s);
       }
       const float w = wpl ? srow[ROWS * 32 - lane] : 0.0f;
+      if (wpl && __float_as_uint(w) != __float_as_uint(w_last)) {
+        // per-edge weight: the products fl(w V'(mu, l)) of this lane's column,
+        // recomputed only when w changes along the line (weight maps are
+        // piecewise constant; bitwise compare, so -0 / NaN never alias)
+        w_last = w;
+#pragma unroll
+        for (int mu = 0; mu < LMAX; ++mu) wv[mu] = fmul(w, vcol[mu]);
+      }
       if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
       // ---- dense min-plus, ascending mu, strict '<': independent chains over
       // mu blocks of 8 (shorter dependency chains), merged in index order with
@@ -169,8 +178,8 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
         const ulonglong2 b4 = *reinterpret_cast<const ulonglong2*>(s_base + m4);
         float v[4];
         if (wpl) {
-          unpack2f(fadd2(b4.x, pack2f(fmul(w, vcol[m4]), fmul(w, vcol[m4 + 1]))), v[0], v[1]);
-          unpack2f(fadd2(b4.y, pack2f(fmul(w, vcol[m4 + 2]), fmul(w, vcol[m4 + 3]))), v[2], v[3]);
+          unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[0], v[1]);
+          unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[2], v[3]);
         } else {
           unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[0], v[1]);
           unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[2], v[3]);

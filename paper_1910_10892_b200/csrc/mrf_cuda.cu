@@ -242,6 +242,13 @@ class FiniteCheck {
     int* host = nullptr;
     int* dev = nullptr;  // device alias of host
     cudaEvent_t done = nullptr;
+    State() = default;
+    State(const State&) = delete;
+    State& operator=(const State&) = delete;
+    ~State() {  // thread exit (errors ignored: the context may already be gone)
+      if (done) cudaEventDestroy(done);
+      if (host) cudaFreeHost(host);
+    }
   };
   static State& state() {
     thread_local std::map<int, State> states;
