@@ -61,7 +61,9 @@ extern "C" {
 
 /* Thread-local description of the last error returned on this thread. */
 const char* mrf_last_error(void);
-/* Library ABI version (major*10000 + minor*100 + patch). */
+/* Library ABI version (major*10000 + minor*100 + patch): 20000 = 2.0.0, the
+ * layout with mrf_problem_f32::assume_finite / diag_gap. */
+#define MRF_VERSION 20000
 int mrf_version(void);
 
 /* ---------------------------------------------------------------- topology */

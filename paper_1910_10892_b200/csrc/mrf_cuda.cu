@@ -505,7 +505,8 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
 extern "C" {
 
 const char* mrf_last_error(void) { return g_last_error.c_str(); }
-int mrf_version(void) { return 100; }
+// 2.0.0: mrf_problem_f32 gained assume_finite and diag_gap (round 2)
+int mrf_version(void) { return 20000; }
 
 int mrf_topology_create(int height, int width, int connectivity, mrf_topology_t* out) {
   return guarded([&] {

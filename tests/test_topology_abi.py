@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.lib()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.mrf_version() >= 100
+    assert lib.mrf_version() == 20000  # MRF_VERSION in include/mrf_cuda.h
 
 
 def test_invalid_arguments_rejected():
