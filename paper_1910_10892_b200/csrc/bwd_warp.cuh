@@ -115,28 +115,40 @@ __global__ void __launch_bounds__(128) bwd_warp_kernel(AccArgs a) {
 #pragma unroll
     for (int rr = 0; rr < NRMAX; ++rr) rowb[rr] = sd[rr] < 0 ? dcb : ainb + size_t(sd[rr] > 0 ? sd[rr] : 0) * NL;
 
-    // node step s (cur = node nsteps - s) into ring slot s % stages
+    // FULL rows: this lane's 16-byte chunk of every staged row and of the p
+    // row at the line's last node step, stepped back one node per issue
+    const float* rsrc[NRMAX + 1];
+#pragma unroll
+    for (int rr = 0; rr <= NRMAX; ++rr)
+      rsrc[rr] = (rr == nrows ? dtsb : rowb[rr < NRMAX ? rr : 0]) + (o_first + nsteps * stL + 4 * lane);
+    const uint8_t* psrc = a.p + size_t(ebase + uint32_t(nsteps - 1)) * L + 16 * lane;
+    int islot = 0;
+    // node step s (cur = node nsteps - s) into ring slot s % stages (issued in order)
     auto issue = [&](int s) {
-      const uint32_t base_s = ring_s + 4u * uint32_t((s % kWarpStages) * stage_f);
+      const uint32_t base_s = ring_s + 4u * uint32_t(islot * stage_f);
+      islot = islot == kWarpStages - 1 ? 0 : islot + 1;
       const int j = nsteps - s;
       const int ocur = o_first + j * stL;
 #pragma unroll
       for (int rr = 0; rr <= NRMAX; ++rr) {
         const bool is_dt = rr == nrows;  // the running dtheta row after the plane rows
         if (rr < nrows || (is_dt && fz)) {
-          const float* src = (is_dt ? dtsb : rowb[rr < NRMAX ? rr : 0]) + ocur;
           if (FULL) {
-#pragma unroll
-            for (int u = lane; u < 8 * EPL; u += 32) cp_async_u32(base_s + 4u * (rr * LS) + 16u * u, src + 4 * u, 16);
+            const uint32_t d = base_s + 4u * (rr * LS) + 16u * lane;
+            if (lane < 8 * EPL) cp_async_u32(d, rsrc[rr], 16);
+            if (lane + 32 < 8 * EPL) cp_async_u32(d + 512u, rsrc[rr] + 128, 16);
           } else if (nvalid > 0) {
+            const float* src = (is_dt ? dtsb : rowb[rr < NRMAX ? rr : 0]) + ocur;
             cp_slice_t<EPL, false>(base_s + 4u * (rr * LS + l0), src + l0, nvalid);
           }
         }
+        if (FULL) rsrc[rr] -= stL;
       }
       const uint32_t e = ebase + uint32_t(j - 1);
       const uint32_t pdst = base_s + 4u * ((NR + 1) * LS);
       if (FULL) {
-        if (lane < 2 * EPL) cp_async_u32(pdst + 16u * lane, a.p + size_t(e) * L + 16 * lane, 16);
+        if (lane < 2 * EPL) cp_async_u32(pdst + 16u * lane, psrc, 16);
+        psrc -= L;
       } else {
         const size_t pb = size_t(e) * L;
         const uint32_t* pwd = reinterpret_cast<const uint32_t*>(a.p) + (pb >> 2);
