@@ -354,27 +354,37 @@ __global__ void __launch_bounds__(32 * (2 + NPRE), MRF_SPLIT_MINB) bwd_split_ker
 
       // this warp's steps: s = pw, pw + NPRE, ...; local index t = s / NPRE
       const int nmine = nsteps > pw ? (nsteps - pw + NPRE - 1) / NPRE : 0;
-      auto issue = [&](int t) {
+      // FULL rows: this lane's 16-byte chunks of the staged rows and of the p
+      // row at this warp's first node step, stepped back NPRE nodes per issue
+      const float* rsrc[NRMAX];
+#pragma unroll
+      for (int rr = 0; rr < NRMAX; ++rr) rsrc[rr] = rowb[rr] + (o_first + (nsteps - pw) * stL + 4 * lane);
+      const uint8_t* psrc = pimg + size_t(ebase + uint32_t(nsteps - pw - 1)) * L + 16 * lane;
+      int islot = 0;
+      auto issue = [&](int t) {  // t = 0, 1, ... in order
         const int s = pw + t * NPRE;
-        const uint32_t base_s = ring_s + 4u * uint32_t((t % kPreStages) * stage_f);
+        const uint32_t base_s = ring_s + 4u * uint32_t(islot * stage_f);
+        islot = islot == kPreStages - 1 ? 0 : islot + 1;
         const int j = nsteps - s;
         const int ocur = o_first + j * stL;
 #pragma unroll
         for (int rr = 0; rr < NRMAX; ++rr) {
           if (rr < nrows) {
-            const float* src = rowb[rr] + ocur;
             if (FULL) {  // the row is 8*EPL 16-byte chunks
-#pragma unroll
-              for (int u = lane; u < 8 * EPL; u += 32) cp_async_u32(base_s + 4u * (rr * LS) + 16u * u, src + 4 * u, 16);
+              const uint32_t d = base_s + 4u * (rr * LS) + 16u * lane;
+              if (lane < 8 * EPL) cp_async_u32(d, rsrc[rr], 16);
+              if (lane + 32 < 8 * EPL) cp_async_u32(d + 512u, rsrc[rr] + 128, 16);
             } else if (nvalid > 0) {
-              cp_slice_t<EPL, false>(base_s + 4u * (rr * LS + l0), src + l0, nvalid);
+              cp_slice_t<EPL, false>(base_s + 4u * (rr * LS + l0), rowb[rr] + ocur + l0, nvalid);
             }
           }
+          if (FULL) rsrc[rr] -= NPRE * stL;
         }
         const uint32_t e = ebase + uint32_t(j - 1);
         const uint32_t pdst = base_s + 4u * (NR * LS);
         if (FULL) {  // p row: 32*EPL bytes at e*L (16 B aligned)
-          if (lane < 2 * EPL) cp_async_u32(pdst + 16u * lane, pimg + size_t(e) * L + 16 * lane, 16);
+          if (lane < 2 * EPL) cp_async_u32(pdst + 16u * lane, psrc, 16);
+          psrc -= NPRE * L;
         } else {
           const size_t pb = size_t(e) * L;
           const uint32_t* pwd = reinterpret_cast<const uint32_t*>(pimg) + (pb >> 2);
