@@ -349,7 +349,13 @@ def main():
     gc = torch.full_like(unary, 1.0 / (wl.N * wl.L))
     # one all-reduce of the packed shared gradient per step, through the
     # library's NCCL collective (mrf_allreduce_grads_f32)
-    comm = NcclComm(dev) if world > 1 else None
+    comm, collective = None, "none (one GPU)"
+    if world > 1:
+        try:
+            comm = NcclComm(dev)
+            collective = "mrf_allreduce_grads_f32 (library NCCL communicator)"
+        except Exception as exc:  # keep the run alive: the same single all-reduce through torch's NCCL
+            collective = f"torch.distributed.all_reduce (library communicator failed: {exc})"
     dp = DataParallelStep(mrf, wl.engine, wl.K, comm=comm)
     fwd_out, grads, shared = dp.fwd, dp.grads, dp.shared
     stream = torch.cuda.current_stream()
@@ -470,7 +476,8 @@ def main():
         "ms_per_image": ms / images * world, "higher_is_better": True,
         "scaling": "strong" if wl.name in GLOBAL_BATCH else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded stereo-like cost volume; no datasets)",
-        "config": config_dict(wl, world, global_batch), "roofline": roof, "e2e": e2e, "gpu_launches": launches,
+        "config": dict(config_dict(wl, world, global_batch), collective=collective), "roofline": roof, "e2e": e2e,
+        "gpu_launches": launches,
         "clocks": clk,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
