@@ -10,6 +10,8 @@
 // reference) and m = out - min.
 #pragma once
 
+#include <type_traits>
+
 #include "fwd_warp.cuh"
 
 namespace mrf {
@@ -34,6 +36,16 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+
+// mu 2^-90 for mu = 0..31 as float pairs: the first-winner key offsets
+// (constant bank, not const: loaded once into uniform registers, which FADD2
+// reads as operands; a const array is folded into per-use UMOVs)
+__constant__ uint64_t kMuKey2[16] = {
+#define MRF_MK(mu) (uint64_t(__builtin_bit_cast(uint32_t, float(mu) * 0x1p-90f)) | \
+                    (uint64_t(__builtin_bit_cast(uint32_t, float(mu + 1) * 0x1p-90f)) << 32))
+    MRF_MK(0),  MRF_MK(2),  MRF_MK(4),  MRF_MK(6),  MRF_MK(8),  MRF_MK(10), MRF_MK(12), MRF_MK(14),
+    MRF_MK(16), MRF_MK(18), MRF_MK(20), MRF_MK(22), MRF_MK(24), MRF_MK(26), MRF_MK(28), MRF_MK(30)};
+#undef MRF_MK
 
 // AGG (TRWP, last sweep only, every node on a line of that direction): the
 // base sum s = theta + sum_d m^d at prev is that node's aggregated cost in
@@ -64,16 +76,21 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
 
   for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
     const LineDesc ld = a.lines[li];
-    const int r = ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
-    const int nsteps = ld.length - 1;
-    if (v_orient != (r & 1)) {  // V'(mu, l) = V(mu, l) (even r) / V(l, mu) (odd r)
-      v_orient = r & 1;
+    if (v_orient != (ld.dir & 1)) {  // V'(mu, l) = V(mu, l) (even r) / V(l, mu) (odd r)
+      v_orient = ld.dir & 1;
 #pragma unroll
       for (int mu = 0; mu < LMAX; ++mu)
         vcol[mu] = mu < L ? __ldg(a.pot.V + (v_orient ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
 #pragma unroll
       for (int mu = 0; mu < LMAX; ++mu) wv[mu] = wpl ? 0.0f : fmul(a.pot.w, vcol[mu]);
     }
+    // the line body with the direction a compile-time constant where TRWP's
+    // addition order depends on it (R == 4: every row offset and select of
+    // the base sum static), else the runtime direction
+    auto sweep = [&](auto rd_tag) {
+    constexpr int RD = decltype(rd_tag)::value;
+    const int r = RD >= 0 ? RD : ld.dir, opp = r ^ 1, st = g.node_step[r], fam = r >> 1;
+    const int nsteps = ld.length - 1;
     float w_last = __uint_as_float(0xffffffffu);  // per-edge w of the cached products: none yet
     const float* rowp[ROWS];
     rowp[0] = un;
@@ -161,44 +178,52 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
         for (int mu = 0; mu < LMAX; ++mu) wv[mu] = fmul(w, vcol[mu]);
       }
       if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
-      // ---- dense min-plus, ascending mu, strict '<': independent chains over
-      // mu blocks of 8 (shorter dependency chains), merged in index order with
-      // the earlier block winning ties. base(mu) comes from a 16-byte
-      // broadcast load of the staged row (4 mu per load), two candidates
-      // share one packed add.
-      constexpr int NB = LMAX / 8;
-      float bb[NB];
-      int ba[NB];
-#pragma unroll
-      for (int c = 0; c < NB; ++c) bb[c] = kInf, ba[c] = 0;
+      // ---- dense min-plus candidates fl(base(mu) + fl(w V'(mu, l))): base(mu)
+      // from a 16-byte broadcast load of the staged row (4 mu per load), two
+      // candidates per packed add
       s_base[lane] = base;
       __syncwarp();
+      float v[LMAX];
 #pragma unroll
       for (int m4 = 0; m4 < LMAX; m4 += 4) {
         const ulonglong2 b4 = *reinterpret_cast<const ulonglong2*>(s_base + m4);
-        float v[4];
-        if (wpl) {
-          unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[0], v[1]);
-          unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[2], v[3]);
-        } else {
-          unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[0], v[1]);
-          unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[2], v[3]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int mu = m4 + u, c = mu / 8;
-          const bool p = v[u] < bb[c];
-          bb[c] = p ? v[u] : bb[c];
-          ba[c] = p ? mu : ba[c];
-        }
+        unpack2f(fadd2(b4.x, pack2f(wv[m4], wv[m4 + 1])), v[m4], v[m4 + 1]);
+        unpack2f(fadd2(b4.y, pack2f(wv[m4 + 2], wv[m4 + 3])), v[m4 + 2], v[m4 + 3]);
       }
-      float best = bb[0];
-      int arg = ba[0];
+      // ---- the reference's ascending strict-'<' scan, restated: its winner is
+      // the FIRST mu whose candidate equals the minimum m (FMNMX3 tree: m is
+      // one of the candidates, bit for bit). For finite |m| >= 2^-60 every
+      // other candidate differs from m by >= 2^-84, so the key fl(fl(v - m) +
+      // mu 2^-90) is exactly mu 2^-90 where v == m and >= 2^-84 elsewhere:
+      // min(key) names the first winner with no per-candidate compare/select
+      // (two packed adds and half an FMNMX3 per candidate, FMA pipe heavy).
+      // m == +-0 (sign of the first winner), +inf / NaN (no winner: label 0,
+      // value +inf) and tiny m take the scan as written.
+      float m0 = v[0], m1 = v[1];
 #pragma unroll
-      for (int c = 1; c < NB; ++c) {
-        const bool p = bb[c] < best;
-        best = p ? bb[c] : best;
-        arg = p ? ba[c] : arg;
+      for (int mu = 2; mu < LMAX; mu += 2) m0 = fminf(m0, v[mu]), m1 = fminf(m1, v[mu + 1]);
+      const float m = fminf(m0, m1);
+      float best;
+      int arg;
+      if (fabsf(m) >= 0x1p-60f && fabsf(m) < kInf) {
+        const uint64_t mneg = pack2f(-m, -m);
+        float k0 = kInf, k1 = kInf;
+#pragma unroll
+        for (int mu = 0; mu < LMAX; mu += 2) {
+          float x, y;
+          unpack2f(fadd2(fadd2(pack2f(v[mu], v[mu + 1]), mneg), kMuKey2[mu / 2]), x, y);
+          k0 = fminf(k0, x), k1 = fminf(k1, y);
+        }
+        arg = int(fmul(fminf(k0, k1), 0x1p90f));
+        best = m;
+      } else {
+        best = kInf, arg = 0;
+#pragma unroll
+        for (int mu = 0; mu < LMAX; ++mu) {
+          const bool p = v[mu] < best;
+          best = p ? v[mu] : best;
+          arg = p ? mu : arg;
+        }
       }
       // ---- p, reparametrisation first argmin (lowest label, -0 as the reference)
       if (valid) *pout = uint8_t(arg);
@@ -223,6 +248,17 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       for (int d = 0; d < R; ++d)
         c = fadd(c, d == r ? carry : (valid ? __ldcg(a.m_in + img + (size_t(d) * N + tail) * L + lane) : 0.0f));
       agg_row(tail, c);
+    }
+    };
+    if constexpr (TRWP && R == 4) {
+      switch (ld.dir) {
+        case 0: sweep(std::integral_constant<int, 0>()); break;
+        case 1: sweep(std::integral_constant<int, 1>()); break;
+        case 2: sweep(std::integral_constant<int, 2>()); break;
+        default: sweep(std::integral_constant<int, 3>()); break;
+      }
+    } else {
+      sweep(std::integral_constant<int, -1>());
     }
     cp_wait<0>();
     __syncwarp();

@@ -126,6 +126,49 @@ def test_c5_shaped_integer_ties():
         assert_forward_equal(f, ref)
 
 
+SMALL_TIES = [
+    # H, W, L, conn, K, kind
+    (9, 11, 21, 4, 3, "int"),
+    (8, 7, 32, 8, 2, "int"),
+    (10, 9, 5, 4, 3, "int"),
+    (9, 11, 21, 4, 2, "tiny"),
+    (7, 8, 16, 4, 2, "huge"),
+]
+
+
+@pytest.mark.parametrize("engine", ["isgmr", "trwp"])
+@pytest.mark.parametrize("case", SMALL_TIES, ids=[f"{c[5]}L{c[2]}c{c[3]}" for c in SMALL_TIES])
+def test_small_label_ties_zeros_and_extremes(engine, case):
+    """The dense small-L forward finds the reference's first strict-'<' winner
+    as the first candidate equal to the minimum, keyed, for finite |min| >=
+    2^-60, and falls back to the scan as written for +-0, tiny and infinite
+    minima (fwd_small.cuh). Integer data (-0 unaries, zero V diagonal, integer
+    weights: exact ties and exact zeros everywhere), values around 2^-60..2^-90
+    and mixed 1e37 / O(1) magnitudes (key differences overflow to +inf) drive
+    every branch."""
+    H, W, L, conn, K, kind = case
+    rng = np.random.default_rng(L * 7 + conn)
+    n = H * W * L
+    if kind == "int":
+        un = -rng.integers(-2, 3, n).astype(np.float32)  # -logits: -0 where the logit is 0
+        V = rng.integers(0, 3, (L, L)).astype(np.float32)
+        np.fill_diagonal(V, 0.0)
+        planes = rng.integers(0, 3, (conn // 2) * H * W).astype(np.float32)
+    elif kind == "tiny":
+        un = (rng.integers(0, 4, n) * 2.0 ** -88).astype(np.float32) * rng.choice([1, -1], n).astype(np.float32)
+        V = (rng.integers(0, 3, (L, L)) * 2.0 ** -89).astype(np.float32)
+        np.fill_diagonal(V, 0.0)
+        planes = rng.choice([0.5, 1.0, 2.0], (conn // 2) * H * W).astype(np.float32)
+    else:
+        un = rng.choice([1e37, 0.0, 3.0, -1e37], n).astype(np.float32)
+        V = rng.choice([0.0, 1e37, 1.0], (L, L)).astype(np.float32)
+        planes = rng.choice([1.0, 3.0], (conn // 2) * H * W).astype(np.float32)
+    pr = O.Problem(H, W, L, conn, un, V.reshape(-1), 1.0, planes, 0.5, None)
+    ref = O.forward(engine, pr, K)
+    f = gpu_forward(engine, to_mrf(pr), K)
+    assert_forward_equal(f, ref)
+
+
 @pytest.mark.parametrize("engine", ["isgmr", "trwp"])
 @pytest.mark.parametrize("shape", [(11, 9, 21, 4, 2, 3), (7, 10, 21, 4, 3, 2), (7, 10, 5, 8, 3, 3),
                                    (7, 10, 192, 4, 3, 2), (5, 8, 30, 4, 1, 3)],
