@@ -82,7 +82,7 @@ static cudaError_t run_split_r(const AccArgs& a, int batch, cudaStream_t s) {
 template <bool TRWP, int RT>
 static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
   const int wpc = 4;
-  const int smem = small_warp_floats(acc_rows(TRWP, a.g.R)) * int(sizeof(float)) * wpc;
+  const int smem = small_cta_floats(acc_rows(TRWP, a.g.R), a.g.L, wpc) * int(sizeof(float));
   auto kern = bwd_small_kernel<TRWP, RT>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
