@@ -24,8 +24,11 @@
 #include "bwd_common.cuh"
 #include "fwd_warp.cuh"
 
+#ifndef MRF_BSMALL_STAGES
+#define MRF_BSMALL_STAGES 3  // cp.async ring depth of the small-L backward (3 vs 4: 7 CTAs per SM at L = 21)
+#endif
 #ifndef MRF_BSMALL_MINB
-#define MRF_BSMALL_MINB 6  // CTAs per SM the register budget is sized for (6 x 4 warps)
+#define MRF_BSMALL_MINB 7  // CTAs per SM the register budget is sized for (7 x 4 warps: 73 registers)
 #endif
 
 namespace mrf {
@@ -34,11 +37,17 @@ namespace mrf {
 // row of 32 floats, p (12 words: L bytes from any offset), {q, w, rho, pad},
 // rho_d[NR]
 __host__ __device__ constexpr int small_stage_floats(int NR) { return ((NR + 1) * 32 + 16 + NR + 3) / 4 * 4; }
-// odd row stride of the per-edge dw parking [32 edges][L labels] (conflict-free both ways)
+constexpr int kSmallStages = MRF_BSMALL_STAGES;
+// per-edge dw terms parked [kPark edges][L labels] with an odd row stride
+// (conflict-free both ways) and summed kPark edges at a time
+constexpr int kPark = 16;
 __host__ __device__ constexpr int small_part_stride(int L) { return L | 1; }
-// per warp: ring + (g, source mask) exchange [64] + dV [L][32] + dw parking [32][L|1]
+// per warp: ring + (g, source mask) exchange [64] + dV [L][32] + dw parking
+// (C4, L = 21: 31.2 KB per 4-warp CTA with 3 ring stages and 16 parked
+// edges: 7 CTAs per SM; 38.5 KB with 4 stages and 32 edges: 5. The kernel is
+// latency-bound, 5 -> 6 -> 7 CTAs took its sweeps 59.2 -> 55.0 -> 53.4 ms per step)
 __host__ __device__ constexpr int small_warp_floats(int NR, int L) {
-  return (kStages * small_stage_floats(NR) + 64 + L * 32 + 32 * small_part_stride(L) + 3) / 4 * 4;
+  return (kSmallStages * small_stage_floats(NR) + 64 + L * 32 + kPark * small_part_stride(L) + 3) / 4 * 4;
 }
 // per CTA: V'(mu, l) of both orientations [2][L][32] (lane l reads column l:
 // conflict-free for any mu), then the warps
@@ -59,10 +68,10 @@ __global__ void __launch_bounds__(128, MRF_BSMALL_MINB) bwd_small_kernel(AccArgs
   const int PS = small_part_stride(L);
   float* s_vall = smem;  // [2][L][32]
   float* ring = smem + 2 * L * 32 + size_t(wid) * small_warp_floats(NR, L);
-  float* s_g = ring + kStages * stage_f;                      // [32] g
+  float* s_g = ring + kSmallStages * stage_f;                      // [32] g
   uint32_t* s_m = reinterpret_cast<uint32_t*>(s_g + 32);      // [32] source masks per target
   float* s_dv = s_g + 64;                                     // [L][32]: (mu, l)
-  float* s_part = s_dv + L * 32;                              // [32][PS] per-edge dw terms
+  float* s_part = s_dv + L * 32;                              // [kPark][PS] per-edge dw terms
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
 
   const int b = blockIdx.y;
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(128, MRF_BSMALL_MINB) bwd_small_kernel(AccArgs
       const size_t pb = pb_i;
       const int cur = cur_i;
       --e_i, pb_i -= L, cur_i -= st;
-      islot = islot == kStages - 1 ? 0 : islot + 1;
+      islot = islot == kSmallStages - 1 ? 0 : islot + 1;
       const uint32_t* pw = reinterpret_cast<const uint32_t*>(pimg + (pb & ~size_t(3)));
       const int nwords = int(((uint32_t(pb) & 3u) + uint32_t(L) + 3u) >> 2);
       const uint32_t pdst = base_s + 4u * ((NR + 1) * 32);
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(128, MRF_BSMALL_MINB) bwd_small_kernel(AccArgs
       }
     };
 #pragma unroll
-    for (int s = 0; s < kStages - 1; ++s) {
+    for (int s = 0; s < kSmallStages - 1; ++s) {
       if (s < nsteps) issue(s);
       cp_commit();
     }
@@ -201,12 +210,12 @@ __global__ void __launch_bounds__(128, MRF_BSMALL_MINB) bwd_small_kernel(AccArgs
     float* aout_p = aoutb + size_t(r) * NL + o_first + (nsteps - 1) * stL;  // A row of step 0's prev
     float* dto_p = fuse ? dthb + o_first + nsteps * stL + lane : nullptr;     // dtheta(cur) of step 0
     for (int s = 0; s < nsteps; ++s) {
-      if (s + kStages - 1 < nsteps) issue(s + kStages - 1);
+      if (s + kSmallStages - 1 < nsteps) issue(s + kSmallStages - 1);
       cp_commit();
-      cp_wait<kStages - 1>();
+      cp_wait<kSmallStages - 1>();
       __syncwarp();  // p / q words were copied by other lanes
       const float* stg = ring + cslot * stage_f;
-      cslot = cslot == kStages - 1 ? 0 : cslot + 1;
+      cslot = cslot == kSmallStages - 1 ? 0 : cslot + 1;
       const int j = nsteps - s;
       const uint32_t e = ebase + uint32_t(j - 1);
       const uint8_t* prow = reinterpret_cast<const uint8_t*>(stg + (NR + 1) * 32) + ((e * uint32_t(L)) & 3u);
@@ -290,12 +299,12 @@ __global__ void __launch_bounds__(128, MRF_BSMALL_MINB) bwd_small_kernel(AccArgs
       // ---- dV (shared accumulator, w folded per edge) and dw of this edge
       if (valid && gl != 0.0f) s_dv[mu * 32 + lane] = fadd(s_dv[mu * 32 + lane], fmul(gl, w));
       if (do_w) {
-        if (valid) s_part[(s & 31) * PS + lane] = gl != 0.0f ? fmul(gl, s_v[mu * 32 + lane]) : 0.0f;
+        if (valid) s_part[(s & (kPark - 1)) * PS + lane] = gl != 0.0f ? fmul(gl, s_v[mu * 32 + lane]) : 0.0f;
         // parked per-edge terms, summed in ascending l by lane e and written
-        // 32 edges at a time (one writer per edge)
-        if ((s & 31) == 31 || s == nsteps - 1) {
+        // kPark edges at a time (one writer per edge)
+        if ((s & (kPark - 1)) == kPark - 1 || s == nsteps - 1) {
           __syncwarp();
-          const int cnt = (s & 31) + 1, s0 = s & ~31;
+          const int cnt = (s & (kPark - 1)) + 1, s0 = s & ~(kPark - 1);
           if (lane < cnt) {
             const float* pr = s_part + lane * PS;
             float part = 0.0f;
