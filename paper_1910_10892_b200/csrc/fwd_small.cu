@@ -8,7 +8,7 @@ template <bool TRWP, int R, int LMAX, bool WPL, bool AGG>
 static cudaError_t run1a(const FwdArgs& a, int batch, cudaStream_t s) {
   constexpr int rows = 1 + (TRWP ? R - 1 : R - 2);
   const int wpc = 4;
-  const int smem = fwd_small_warp_floats(rows, kStages) * int(sizeof(float)) * wpc;
+  const int smem = fwd_small_warp_floats(rows, kStages, WPL ? LMAX : 0) * int(sizeof(float)) * wpc;
   auto kern = fwd_small_kernel<TRWP, R, LMAX, WPL, AGG>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;

@@ -19,7 +19,11 @@ namespace mrf {
 // per-warp ring stage: ROWS rows of 32 floats + {w, rho}, padded to 16 B
 __host__ __device__ constexpr int fwd_small_stage(int rows) { return rows * 32 + 4; }
 // per-warp floats: the ring + base(mu) of the current node (32, 16 B aligned)
-__host__ __device__ constexpr int fwd_small_warp_floats(int rows, int stages) { return stages * fwd_small_stage(rows) + 32; }
+// + with per-edge weights the lane's V' column [LMAX][32] (read only when w
+// changes: 24 registers fewer in the node loop)
+__host__ __device__ constexpr int fwd_small_warp_floats(int rows, int stages, int vcols = 0) {
+  return stages * fwd_small_stage(rows) + 32 + vcols * 32;
+}
 
 __device__ __forceinline__ uint64_t pack2f(float x, float y) {
   uint64_t r;
@@ -61,8 +65,9 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
   const Geometry& g = a.g;
   const int L = g.L, N = g.N;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
-  float* ring = smem + size_t(wid) * fwd_small_warp_floats(ROWS, kStages);
+  float* ring = smem + size_t(wid) * fwd_small_warp_floats(ROWS, kStages, WPL ? LMAX : 0);
   float* s_base = ring + kStages * STG;  // base(mu) of the current node, broadcast to every label
+  float* s_vcol = s_base + 32;           // WPL: V'(mu, lane) at [mu][lane]
   const uint32_t ring_s = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
   const int b = blockIdx.y;
   const bool valid = lane < L;
@@ -72,17 +77,18 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
   const bool rpl = TRWP && a.pot.rho_planes != nullptr;
   const int l = valid ? lane : 0;
   int v_orient = -1;
-  float vcol[LMAX], wv[LMAX];
+  float wv[LMAX];
 
   for (int li = blockIdx.x * wpc + wid; li < a.nlines; li += gridDim.x * wpc) {
     const LineDesc ld = a.lines[li];
     if (v_orient != (ld.dir & 1)) {  // V'(mu, l) = V(mu, l) (even r) / V(l, mu) (odd r)
       v_orient = ld.dir & 1;
 #pragma unroll
-      for (int mu = 0; mu < LMAX; ++mu)
-        vcol[mu] = mu < L ? __ldg(a.pot.V + (v_orient ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
-#pragma unroll
-      for (int mu = 0; mu < LMAX; ++mu) wv[mu] = wpl ? 0.0f : fmul(a.pot.w, vcol[mu]);
+      for (int mu = 0; mu < LMAX; ++mu) {
+        const float vc = mu < L ? __ldg(a.pot.V + (v_orient ? size_t(l) * L + mu : size_t(mu) * L + l)) : 0.0f;
+        if (wpl) s_vcol[mu * 32 + lane] = vc;
+        wv[mu] = wpl ? 0.0f : fmul(a.pot.w, vc);
+      }
     }
     // the line body with the direction a compile-time constant where TRWP's
     // addition order depends on it (R == 4: every row offset and select of
@@ -175,7 +181,7 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
         // piecewise constant; bitwise compare, so -0 / NaN never alias)
         w_last = w;
 #pragma unroll
-        for (int mu = 0; mu < LMAX; ++mu) wv[mu] = fmul(w, vcol[mu]);
+        for (int mu = 0; mu < LMAX; ++mu) wv[mu] = fmul(w, s_vcol[mu * 32 + lane]);
       }
       if (!valid) base = kInf;  // labels >= L never win (their V' column is 0)
       // ---- dense min-plus candidates fl(base(mu) + fl(w V'(mu, l))): base(mu)
