@@ -41,6 +41,23 @@ __device__ __forceinline__ float plane_value(const float* planes, float c, int N
 // Monotone float -> uint32 map (non-NaN inputs). -0 is folded onto +0 by the
 // caller (v + 0.0f) so that equal values compare equal, as the reference's
 // strict '<' scans treat them.
+// packed f32x2 helpers (FADD2)
+__device__ __forceinline__ uint64_t pack2f(float x, float y) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void unpack2f(uint64_t v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+// two IEEE round-to-nearest adds in one FADD2 (products stay scalar: ptxas
+// would contract mul.rn.f32x2 + add.rn.f32x2 into FFMA2)
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t order_key(float v) {
   const uint32_t u = __float_as_uint(v);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);

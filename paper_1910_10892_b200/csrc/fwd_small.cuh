@@ -25,22 +25,6 @@ __host__ __device__ constexpr int fwd_small_warp_floats(int rows, int stages, in
   return stages * fwd_small_stage(rows) + 32 + vcols * 32;
 }
 
-__device__ __forceinline__ uint64_t pack2f(float x, float y) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
-  return r;
-}
-__device__ __forceinline__ void unpack2f(uint64_t v, float& x, float& y) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
-}
-// two IEEE round-to-nearest adds in one FADD2 (products stay scalar: ptxas
-// would contract mul.rn.f32x2 + add.rn.f32x2 into FFMA2)
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-
 // mu 2^-90 for mu = 0..31 as float pairs: the first-winner key offsets
 // (constant bank, not const: loaded once into uniform registers, which FADD2
 // reads as operands; a const array is folded into per-use UMOVs)
