@@ -194,8 +194,9 @@ def host_info(threads: int) -> dict:
                 model = ln.split(":", 1)[1].strip()
     except Exception:
         pass
+    # threads == 0 is the reference's parallel_for default: every hardware thread
     return {"nproc": os.cpu_count(), "cpu_model": model, "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
-            "threads_used": threads}
+            "threads_used": threads if threads > 0 else os.cpu_count()}
 
 
 def cpu_reference_run(wl, K: int, rows: int | None = None, threads: int = 0):
