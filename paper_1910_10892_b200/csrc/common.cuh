@@ -58,6 +58,15 @@ __device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
   return r;
 }
 
+// warp-wide minimum of a float in one CREDUX.MIN.F32 (sm_100a); callers pass
+// no NaN and no -0 (values normalised by +0 where a -0 can occur), so the
+// result equals the order-key minimum bit for bit
+__device__ __forceinline__ float warp_min_f32(float v) {
+  float r;
+  asm volatile("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t order_key(float v) {
   const uint32_t u = __float_as_uint(v);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);

@@ -449,10 +449,8 @@ __global__ void __launch_bounds__(128) fwd_band2_kernel(FwdArgs a) {
       int lidx = l0 + EPL - 1;
 #pragma unroll
       for (int i = EPL - 2; i >= 0; --i) lidx = out[i] == lm ? l0 + i : lidx;
-      const uint32_t lk = order_key(lm);
-      const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
-      const uint32_t qmin = __reduce_min_sync(0xffffffffu, lk == kmin ? uint32_t(lidx) : 0xffffffffu);
-      const float lo = key_value(kmin);
+      const float lo = warp_min_f32(lm);
+      const uint32_t qmin = __reduce_min_sync(0xffffffffu, lm == lo ? uint32_t(lidx) : 0xffffffffu);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) carry[i] = fsub(out[i], lo);
       const int cur = ld.first + j * st;

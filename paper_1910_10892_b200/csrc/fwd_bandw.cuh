@@ -256,18 +256,16 @@ __global__ void __launch_bounds__(128) fwd_bandw_kernel(FwdArgs a) {
 
       // ---- p row, reparametrisation (first argmin; banded values are never -0)
       store_p<EPL, FULL>(a.p + (pq_base + j - 1) * L, l0, am, nvalid);
-      uint32_t lk = order_key(out[0]);
-      int lidx = l0;
+      // lane minimum by fminf (exact: no candidate is NaN or -0, PairDesc),
+      // its first position by equality, scanning down
+      float lm = out[0];
 #pragma unroll
-      for (int i = 1; i < EPL; ++i) {
-        const uint32_t kk = order_key(out[i]);
-        const bool t = kk < lk;
-        lk = t ? kk : lk;
-        lidx = t ? l0 + i : lidx;
-      }
-      const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
-      const uint32_t qmin = __reduce_min_sync(0xffffffffu, lk == kmin ? uint32_t(lidx) : 0xffffffffu);
-      const float lo = key_value(kmin);
+      for (int i = 1; i < EPL; ++i) lm = fminf(lm, out[i]);
+      int lidx = l0 + EPL - 1;
+#pragma unroll
+      for (int i = EPL - 2; i >= 0; --i) lidx = out[i] == lm ? l0 + i : lidx;
+      const float lo = warp_min_f32(lm);
+      const uint32_t qmin = __reduce_min_sync(0xffffffffu, lm == lo ? uint32_t(lidx) : 0xffffffffu);
 #pragma unroll
       for (int i = 0; i < EPL; ++i) carry[i] = fsub(out[i], lo);
       const int cur = ld.first + j * st;

@@ -127,9 +127,9 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
     auto agg_row = [&](int n, float c) {
       const size_t nb = size_t(b) * N + n;
       if (a.agg_cost && valid) a.agg_cost[nb * L + lane] = c;
-      const uint32_t kk = valid ? order_key(fadd(c, 0.0f)) : 0xffffffffu;
-      const uint32_t kmin = __reduce_min_sync(0xffffffffu, kk);
-      const uint32_t lmin = __reduce_min_sync(0xffffffffu, kk == kmin ? uint32_t(lane) : 0xffffffffu);
+      const float cn = valid ? fadd(c, 0.0f) : kInf;
+      const float cmin = warp_min_f32(cn);
+      const uint32_t lmin = __reduce_min_sync(0xffffffffu, cn == cmin ? uint32_t(lane) : 0xffffffffu);
       if (lane == 0 && a.agg_labels) a.agg_labels[nb] = uint16_t(lmin);
     };
 
@@ -218,12 +218,11 @@ __global__ void __launch_bounds__(128) fwd_small_kernel(FwdArgs a) {
       // ---- p, reparametrisation first argmin (lowest label, -0 as the reference)
       if (valid) *pout = uint8_t(arg);
       pout += L;
-      const uint32_t lk = valid ? order_key(fadd(best, 0.0f)) : 0xffffffffu;
+      const float bn = valid ? fadd(best, 0.0f) : kInf;  // -0 -> +0: no -0 reaches the float minimum
       const uint32_t lt = valid ? (uint32_t(lane) << 1) | (__float_as_uint(best) == 0x80000000u ? 1u : 0u) : 0xffffffffu;
-      const uint32_t kmin = __reduce_min_sync(0xffffffffu, lk);
-      const uint32_t tmin = __reduce_min_sync(0xffffffffu, lk == kmin ? lt : 0xffffffffu);
-      float lo = key_value(kmin);
-      if (tmin & 1u) lo = -0.0f;
+      const float bmin = warp_min_f32(bn);
+      const uint32_t tmin = __reduce_min_sync(0xffffffffu, bn == bmin ? lt : 0xffffffffu);
+      const float lo = (tmin & 1u) ? -0.0f : bmin;
       carry = fsub(best, lo);
       if (valid) *mout = carry;
       mout += row_step;
