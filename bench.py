@@ -451,7 +451,7 @@ def main():
 
     fwd_roof = kernel_roof("fwd sweep (min-plus + argmin, stored indices)", f_sw, f_nl, f_launch_ms,
                            fwd_ms / max(ms, 1e-9), "fwd")
-    bwd_roof = kernel_roof("bwd sweep (index-driven scatter, bwd_split / bwd_small)", b_sw, b_nl, b_launch_ms,
+    bwd_roof = kernel_roof("bwd sweep (index-driven scatter: bwd_split / bwd_warp / bwd_small / bwd_grp by config)", b_sw, b_nl, b_launch_ms,
                            bwd_ms / max(ms, 1e-9), "bwd")
     roof = dict(bwd_roof if bwd_ms >= fwd_ms else fwd_roof)
     roof["other_kernel"] = fwd_roof if bwd_ms >= fwd_ms else bwd_roof

@@ -3,6 +3,7 @@
 #pragma once
 
 #include "bwd_common.cuh"
+#include "bwd_grp.cuh"
 #include "bwd_small.cuh"
 #include "bwd_split.cuh"
 #include "bwd_warp.cuh"
@@ -93,9 +94,32 @@ static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// TRWP-4, 16 < L <= 24, constant rho, unary gradient not fused: 8 lanes x 3
+// labels per line, 4 lines per warp (bwd_grp.cuh); one private dV slot per
+// line group, at most kDvSlotsSmall per image
+static cudaError_t run_grp(const AccArgs& a, int batch, cudaStream_t s) {
+  const int wpc = kBgWarps;
+  const int smem = bwd_grp_cta_floats(wpc) * int(sizeof(float));
+  auto kern = bwd_grp_kernel<0>;
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
+  if (e != cudaSuccess) return e;
+  const int per_cta = wpc * kGrpLines;
+  const int want = (a.nlines + per_cta - 1) / per_cta;
+  const int cap = kDvSlotsSmall / per_cta;
+  kern<<<dim3(want < cap ? want : cap, batch), 32 * wpc, smem, s>>>(a); note_launch();
+  return cudaGetLastError();
+}
+
+inline bool bwd_grp_applies(const AccArgs& a) {
+  const char* env = getenv("MRF_BWD_GRP");  // A/B: 0 = lane-per-label kernel only
+  if (env && env[0] == '0') return false;
+  return a.g.R == 4 && a.g.L > 16 && a.g.L <= 24 && a.pot.rho_planes == nullptr && a.dtheta == nullptr;
+}
+
 template <bool TRWP>
 static cudaError_t launch_bwd_sweep(const AccArgs& a, int batch, cudaStream_t s) {
   if (a.nlines == 0) return cudaSuccess;
+  if (TRWP && bwd_uses_small(a.g.L, a.nlines, batch) && bwd_grp_applies(a)) return run_grp(a, batch, s);
   // L <= 32 with many lines: one warp per line; few lines: warp-specialised
   if (bwd_uses_small(a.g.L, a.nlines, batch)) {
     if (a.g.R == 4) return run_small<TRWP, 4>(a, batch, s);

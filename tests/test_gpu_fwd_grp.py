@@ -48,3 +48,49 @@ def test_grouped_small_forward_batch_seg():
     f = gpu_forward("trwp", to_mrf(prs[0], batch_unary=list(wl.unary), batch_wplanes=list(wl.w_planes)), K)
     for b in range(B):
         assert_forward_equal(f, O.forward("trwp", prs[b], K), b=b)
+
+
+BWD_CASES = [
+    # H, W, L, K, per-edge w, batch
+    (9, 11, 21, 3, True, 3),
+    (13, 6, 17, 2, False, 2),
+    (7, 10, 24, 3, True, 2),
+    (1, 12, 21, 2, False, 1),
+    (23, 18, 21, 4, True, 2),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("grp", ["1", "0"], ids=["grouped", "lane_per_label"])
+@pytest.mark.parametrize("case", BWD_CASES, ids=[f"{c[0]}x{c[1]}L{c[2]}K{c[3]}B{c[5]}{'w' if c[4] else ''}" for c in BWD_CASES])
+def test_grouped_small_backward(case, grp, monkeypatch):
+    """The grouped small-L TRWP-4 backward (bwd_grp.cuh) against the reference
+    restatement within 1e-5 (normwise and elementwise), and bit-identical run
+    to run; MRF_BWD_SMALL=1 puts these few-line launches on the small-L
+    kernels, MRF_BWD_GRP=0 on the lane-per-label one it replaces."""
+    import torch
+    from tests.gpu_util import assert_grads_close, gpu_backward
+    monkeypatch.setenv("MRF_BWD_SMALL", "1")
+    monkeypatch.setenv("MRF_BWD_GRP", grp)
+    H, W, L, K, per_edge, B = case
+    uns, pls, prs = [], [], []
+    V = wc0 = None
+    for b in range(B):  # V and a constant weight are shared by the batch
+        un, V0, wc, planes = WL.random_problem(H, W, L, 4, seed=H * 7 + W + L + b, per_edge=per_edge)
+        V = V0 if V is None else V
+        wc0 = wc if wc0 is None else wc0
+        uns.append(un)
+        pls.append(planes)
+        prs.append(O.Problem(H, W, L, 4, un, V, wc0, planes, 0.5, None))
+    mrf = to_mrf(prs[0], batch_unary=uns, batch_wplanes=pls if per_edge else None)
+    f = gpu_forward("trwp", mrf, K)
+    gcs = np.random.default_rng(L + K).normal(size=(B, H * W * L)).astype(np.float32)
+    g = gpu_backward("trwp", mrf, f, gcs)
+    for b in range(B):
+        ref = O.forward("trwp", prs[b], K)
+        assert_forward_equal(f, ref, b=b)
+        assert_grads_close(g, O.backward("trwp", prs[b], K, ref.p, ref.q, gcs[b]), b=b)
+    g2 = gpu_backward("trwp", mrf, f, gcs)
+    assert torch.equal(g.pairwise, g2.pairwise) and torch.equal(g.unary, g2.unary)
+    if g.edge_weights is not None:
+        assert torch.equal(g.edge_weights, g2.edge_weights)
