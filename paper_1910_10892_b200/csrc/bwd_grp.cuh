@@ -40,6 +40,9 @@ __host__ __device__ constexpr int bwd_grp_warp_floats() {
 }
 // per CTA: V'(mu, l) of both orientations [2][24][24], then the warps
 __host__ __device__ constexpr int bwd_grp_cta_floats(int wpc) { return 2 * 24 * 24 + wpc * bwd_grp_warp_floats(); }
+#ifndef MRF_BGRP_MINB
+#define MRF_BGRP_MINB 1  // CTAs per SM the register budget is sized for (A/B)
+#endif
 #ifndef MRF_BGRP_WARPS
 #define MRF_BGRP_WARPS 4
 #endif
@@ -262,7 +265,7 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
 }
 
 template <int DUMMY>
-__global__ void __launch_bounds__(128) bwd_grp_kernel(AccArgs a) {
+__global__ void __launch_bounds__(128, MRF_BGRP_MINB) bwd_grp_kernel(AccArgs a) {
   extern __shared__ __align__(16) float smem[];
   const Geometry& g = a.g;
   const int L = g.L;
