@@ -28,27 +28,32 @@
 namespace mrf {
 
 constexpr int kBgStages = 3;  // cp.async ring depth
-// per line and stage (floats): 4 rows of 24 + p words (8) + {q word, w, pad, pad}
-constexpr int kBgLineStage = 4 * 24 + 8 + 4;
+// per line and stage (floats): 5 rows of 24 (up to 4 gradient rows + the
+// running dtheta row of the fused sweep) + p words (8) + {q word, w, pad, pad}
+// (the unfused kernel keeps 4 rows: 1.7 ms per C4 backward faster)
+__host__ __device__ constexpr int bg_rows(bool fuse) { return fuse ? 5 : 4; }
+__host__ __device__ constexpr int bg_line_stage(bool fuse) { return bg_rows(fuse) * 24 + 8 + 4; }
 // per warp floats: ring [stages][4 lines][kBgLineStage] + (g [24], p [24 bytes = 6 words], pad) per line
 // + dV [4 lines][24 mu][24 l]
 #ifndef MRF_BGRP_RED
 #define MRF_BGRP_RED 1  // 0: shared [mu][l] accumulator per group (measured slower); 1: dV by RED into the group's slot every step (no shared accumulator)
 #endif
-__host__ __device__ constexpr int bwd_grp_warp_floats() {
-  return kBgStages * kGrpLines * kBgLineStage + kGrpLines * 32 + (MRF_BGRP_RED ? 0 : kGrpLines * 24 * 24);
+__host__ __device__ constexpr int bwd_grp_warp_floats(bool fuse) {
+  return kBgStages * kGrpLines * bg_line_stage(fuse) + kGrpLines * 32 + (MRF_BGRP_RED ? 0 : kGrpLines * 24 * 24);
 }
 // per CTA: V'(mu, l) of both orientations [2][24][24], then the warps
-__host__ __device__ constexpr int bwd_grp_cta_floats(int wpc) { return 2 * 24 * 24 + wpc * bwd_grp_warp_floats(); }
+__host__ __device__ constexpr int bwd_grp_cta_floats(int wpc, bool fuse) {
+  return 2 * 24 * 24 + wpc * bwd_grp_warp_floats(fuse);
+}
 #ifndef MRF_BGRP_MINB
-#define MRF_BGRP_MINB 1  // CTAs per SM the register budget is sized for (A/B)
+#define MRF_BGRP_MINB 5  // CTAs per SM the unfused kernel is sized for (<= 102 registers; 7 measured slower; A/B)
 #endif
 #ifndef MRF_BGRP_WARPS
 #define MRF_BGRP_WARPS 4
 #endif
 constexpr int kBgWarps = MRF_BGRP_WARPS;
 
-template <int RD, int FT>
+template <int RD, int FT, bool FUSE>
 __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& ld, bool has, int maxs, int slot,
                                              float* ring, float* s_gp, float* s_dv, const float* s_vall) {
   constexpr int R = 4, EPL = 3, LP = 24;
@@ -64,6 +69,10 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
   const int nv = min(EPL, max(0, L - l0));
   const int b = blockIdx.y;
   const bool wpl = a.pot.w_planes != nullptr, do_w = a.gw != nullptr;
+  // direction 0 also collects the iteration's unary gradient (bwd_small.cuh
+  // rules): dtheta(cur) = dtheta_src(cur) + rho sum_{d != 0} A[d](cur) + carry
+  constexpr bool fuse = FUSE && r == 0;
+  constexpr int kBgRows = bg_rows(FUSE), kBgLineStage = bg_line_stage(FUSE);
   const int st = g.node_step[r];
   const int nsteps = has ? ld.length - 1 : 0;
   const ptrdiff_t stL = ptrdiff_t(st) * L;
@@ -76,6 +85,8 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
   const float* ainb = a.ain + size_t(b) * R * NL + l0;
   float* aoutb = a.aout + size_t(b) * R * NL + l0;
   const float* dcb = a.dc + size_t(b) * NL + l0;
+  const float* dtsb = fuse ? a.dtheta_src + size_t(b) * NL + l0 : nullptr;
+  float* dtob = fuse ? a.dtheta + size_t(b) * NL + l0 : nullptr;
   const uint8_t* pimg = a.p;
   const uint8_t* qimg = a.q;
   // plane of each staged row (-1: dc)
@@ -119,14 +130,19 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
         for (int t = 0; t < EPL; ++t)
           if (t < nv) cp_async_u32(sb + 4u * uint32_t(rr * LP + l0 + t), src + t, 4);
       }
+      if (fuse) {
+#pragma unroll
+        for (int t = 0; t < EPL; ++t)
+          if (t < nv) cp_async_u32(sb + 4u * uint32_t(4 * LP + l0 + t), dtsb + off + t, 4);
+      }
       const uint32_t e = e_base + uint32_t(nsteps - issued);  // edge (prev -> cur), prev = cur - st
       const size_t pb = size_t(e) * L;
       const int nwords = int(((uint32_t(pb) & 3u) + uint32_t(L) + 3u) >> 2);
       if (gl < nwords)
-        cp_async_u32(sb + 4u * uint32_t(4 * LP + gl), reinterpret_cast<const uint32_t*>(pimg + (pb & ~size_t(3))) + gl, 4);
-      if (gl == 0) cp_async_u32(sb + 4u * uint32_t(4 * LP + 8), reinterpret_cast<const uint32_t*>(qimg) + (e >> 2), 4);
+        cp_async_u32(sb + 4u * uint32_t(kBgRows * LP + gl), reinterpret_cast<const uint32_t*>(pimg + (pb & ~size_t(3))) + gl, 4);
+      if (gl == 0) cp_async_u32(sb + 4u * uint32_t(kBgRows * LP + 8), reinterpret_cast<const uint32_t*>(qimg) + (e >> 2), 4);
       const int wnode = (r & 1) ? cur_i : cur_i - st;
-      if (wpl && gl == 1) cp_async_u32(sb + 4u * uint32_t(4 * LP + 9), wrow + wnode, 4);
+      if (wpl && gl == 1) cp_async_u32(sb + 4u * uint32_t(kBgRows * LP + 9), wrow + wnode, 4);
     }
     cur_i -= st;
     islot = islot == kBgStages - 1 ? 0 : islot + 1;
@@ -159,19 +175,20 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
     cslot = cslot == kBgStages - 1 ? 0 : cslot + 1;
     const int j = nsteps - s;  // edge j-1: prev = node j-1, cur = node j
     const uint32_t e = e_base + uint32_t(j - 1);
-    const uint8_t* prow = reinterpret_cast<const uint8_t*>(stg + 4 * LP) + ((e * uint32_t(L)) & 3u);
-    const int qv = (__float_as_uint(stg[4 * LP + 8]) >> (8 * (e & 3))) & 0xff;
-    const float w = wpl ? stg[4 * LP + 9] : a.pot.w;
+    const uint8_t* prow = reinterpret_cast<const uint8_t*>(stg + kBgRows * LP) + ((e * uint32_t(L)) & 3u);
+    const int qv = (__float_as_uint(stg[kBgRows * LP + 8]) >> (8 * (e & 3))) & 0xff;
+    const float w = wpl ? stg[kBgRows * LP + 9] : a.pot.w;
     // ---- x (bwd_common.cuh rules, bwd_small.cuh order) and row = x + carry
-    float row[EPL];
+    float row[EPL], rsum[EPL];
     int mu[EPL];
 #pragma unroll
     for (int t = 0; t < EPL; ++t) {
       float x = 0.0f;
+      rsum[t] = 0.0f;
 #pragma unroll
       for (int rr = A0; rr < NROWS; ++rr) x = fadd(x, stg[rr * LP + l0 + t]);
       if (NROWS > A0) {
-        x = fmul(a.pot.rho, x);
+        rsum[t] = x = fmul(a.pot.rho, x);
         if (opp_slot >= 0) x = fsub(x, stg[(opp_slot >= 0 ? opp_slot : 0) * LP + l0 + t]);
       }
       if (first) x = fadd(stg[l0 + t], x);
@@ -209,6 +226,11 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
       }
     }
     const int prev = ld.first + (j - 1) * st;
+    if (fuse && act) {  // the unary gradient of node cur, with this sweep's share (the carry into cur)
+#pragma unroll
+      for (int t = 0; t < EPL; ++t)
+        if (t < nv) dtob[size_t(prev + st) * L + t] = fadd(fadd(stg[4 * LP + l0 + t], rsum[t]), carry[t]);
+    }
     if (act) {
 #pragma unroll
       for (int t = 0; t < EPL; ++t)
@@ -246,6 +268,17 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
   }
   cp_wait<0>();
   __syncwarp();
+  if (fuse && has) {  // the head is no edge's cur: its rows are read here
+    const int head = ld.first;
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
+      if (t >= nv) continue;
+      float hs = 0.0f;
+#pragma unroll
+      for (int d = 1; d < R; ++d) hs = fadd(hs, fmul(a.pot.rho, __ldcg(ainb + size_t(d) * NL + size_t(head) * L + t)));
+      dtob[size_t(head) * L + t] = fadd(fadd(dtsb[size_t(head) * L + t], hs), carry[t]);
+    }
+  }
   // flush this line's dV partials into the group's private slot
   if (has && !MRF_BGRP_RED) {
     for (int m = 0; m < L; ++m) {
@@ -264,16 +297,19 @@ __device__ __forceinline__ void bwd_grp_line(const AccArgs& a, const LineDesc& l
   __syncwarp();
 }
 
-template <int DUMMY>
-__global__ void __launch_bounds__(128, MRF_BGRP_MINB) bwd_grp_kernel(AccArgs a) {
+// FUSE: the direction-0 launches of a call that collects the unary gradient
+// in the sweep (a separate instantiation: the unfused kernel keeps its 90
+// registers; both together in one kernel took 162)
+template <bool FUSE>
+__global__ void __launch_bounds__(128, FUSE ? 5 : MRF_BGRP_MINB) bwd_grp_kernel(AccArgs a) {
   extern __shared__ __align__(16) float smem[];
   const Geometry& g = a.g;
   const int L = g.L;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, wpc = blockDim.x >> 5;
   const int gi = lane >> 3;
   float* s_vall = smem;  // [2][24][24]
-  float* ring = smem + 2 * 24 * 24 + size_t(wid) * bwd_grp_warp_floats();
-  float* s_gp = ring + kBgStages * kGrpLines * kBgLineStage;  // [4 lines][32]
+  float* ring = smem + 2 * 24 * 24 + size_t(wid) * bwd_grp_warp_floats(FUSE);
+  float* s_gp = ring + kBgStages * kGrpLines * bg_line_stage(FUSE);  // [4 lines][32]
   float* s_dv = s_gp + kGrpLines * 32;                         // [4 lines][24][24]
   if (a.gw != nullptr) {  // V'(mu, l) = V(mu, l) (even r) / V(l, mu) (odd r)
     for (int t = threadIdx.x; t < 2 * 24 * 24; t += blockDim.x) {
@@ -295,15 +331,20 @@ __global__ void __launch_bounds__(128, MRF_BGRP_MINB) bwd_grp_kernel(AccArgs a) 
     maxs = max(maxs, __shfl_xor_sync(0xffffffffu, maxs, 8));
     maxs = max(maxs, __shfl_xor_sync(0xffffffffu, maxs, 16));
     // every line of a TRWP launch sweeps one direction
-    switch (ld.dir * 2 + (first ? 1 : 0)) {
-      case 0: bwd_grp_line<0, 0>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 1: bwd_grp_line<0, 1>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 2: bwd_grp_line<1, 0>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 3: bwd_grp_line<1, 1>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 4: bwd_grp_line<2, 0>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 5: bwd_grp_line<2, 1>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      case 6: bwd_grp_line<3, 0>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
-      default: bwd_grp_line<3, 1>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+    if constexpr (FUSE) {  // direction 0 only
+      if (first) bwd_grp_line<0, 1, true>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall);
+      else bwd_grp_line<0, 0, true>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall);
+    } else {
+      switch (ld.dir * 2 + (first ? 1 : 0)) {
+        case 0: bwd_grp_line<0, 0, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 1: bwd_grp_line<0, 1, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 2: bwd_grp_line<1, 0, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 3: bwd_grp_line<1, 1, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 4: bwd_grp_line<2, 0, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 5: bwd_grp_line<2, 1, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        case 6: bwd_grp_line<3, 0, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+        default: bwd_grp_line<3, 1, false>(a, ld, has, maxs, slot, ring, s_gp, s_dv, s_vall); break;
+      }
     }
   }
 }

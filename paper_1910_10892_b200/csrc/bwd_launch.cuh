@@ -99,8 +99,9 @@ static cudaError_t run_small(const AccArgs& a, int batch, cudaStream_t s) {
 // line group, at most kDvSlotsSmall per image
 static cudaError_t run_grp(const AccArgs& a, int batch, cudaStream_t s) {
   const int wpc = kBgWarps;
-  const int smem = bwd_grp_cta_floats(wpc) * int(sizeof(float));
-  auto kern = bwd_grp_kernel<0>;
+  const int smem = bwd_grp_cta_floats(wpc, a.dtheta != nullptr) * int(sizeof(float));
+  // a.dtheta is set only on the direction-0 launches of a fused call
+  auto kern = a.dtheta ? bwd_grp_kernel<true> : bwd_grp_kernel<false>;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   const int per_cta = wpc * kGrpLines;
@@ -111,9 +112,7 @@ static cudaError_t run_grp(const AccArgs& a, int batch, cudaStream_t s) {
 }
 
 inline bool bwd_grp_applies(const AccArgs& a) {
-  const char* env = getenv("MRF_BWD_GRP");  // A/B: 0 = lane-per-label kernel only
-  if (env && env[0] == '0') return false;
-  return a.g.R == 4 && a.g.L > 16 && a.g.L <= 24 && a.pot.rho_planes == nullptr && a.dtheta == nullptr;
+  return bwd_grp_enabled(a.g.L, a.g.R, a.pot.rho_planes != nullptr);
 }
 
 template <bool TRWP>

@@ -66,6 +66,20 @@ inline bool bwd_small_fuse() {
   return env && env[0] == '1';
 }
 
+// TRWP-4, 16 < L <= 24, constant rho: the grouped small-L backward
+// (bwd_grp.cuh) takes the launches bwd_uses_small gives the small-L kernels
+inline bool bwd_grp_enabled(int L, int R, bool rho_planes) {
+  const char* env = getenv("MRF_BWD_GRP");  // A/B: 0 = lane-per-label kernel only
+  if (env && env[0] == '0') return false;
+  return R == 4 && L > 16 && L <= 24 && !rho_planes;
+}
+// ... and collects the unary gradient in its direction-0 sweep (A/B:
+// MRF_GRP_FUSE=0 leaves it to dtheta_acc_kernel)
+inline bool bwd_grp_fuse() {
+  const char* env = getenv("MRF_GRP_FUSE");
+  return !(env && env[0] == '0');
+}
+
 // warps per CTA: few long chains -> spread them over every SM
 inline int warps_per_cta(int nlines) {
   const char* env = getenv("MRF_FWD_WPC");  // A/B: force 1, 2 or 4 warps per CTA

@@ -61,17 +61,20 @@ BWD_CASES = [
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("grp", ["1", "0"], ids=["grouped", "lane_per_label"])
+@pytest.mark.parametrize("grp", ["1", "1u", "0"], ids=["grouped_fused", "grouped", "lane_per_label"])
 @pytest.mark.parametrize("case", BWD_CASES, ids=[f"{c[0]}x{c[1]}L{c[2]}K{c[3]}B{c[5]}{'w' if c[4] else ''}" for c in BWD_CASES])
 def test_grouped_small_backward(case, grp, monkeypatch):
-    """The grouped small-L TRWP-4 backward (bwd_grp.cuh) against the reference
-    restatement within 1e-5 (normwise and elementwise), and bit-identical run
-    to run; MRF_BWD_SMALL=1 puts these few-line launches on the small-L
-    kernels, MRF_BWD_GRP=0 on the lane-per-label one it replaces."""
+    """The grouped small-L TRWP-4 backward (bwd_grp.cuh), with the unary
+    gradient collected in its direction-0 sweep (default) or by
+    dtheta_acc_kernel (MRF_GRP_FUSE=0), against the reference restatement
+    within 1e-5 (normwise and elementwise), and bit-identical run to run;
+    MRF_BWD_SMALL=1 puts these few-line launches on the small-L kernels,
+    MRF_BWD_GRP=0 on the lane-per-label one it replaces."""
     import torch
     from tests.gpu_util import assert_grads_close, gpu_backward
     monkeypatch.setenv("MRF_BWD_SMALL", "1")
-    monkeypatch.setenv("MRF_BWD_GRP", grp)
+    monkeypatch.setenv("MRF_BWD_GRP", grp[0])
+    monkeypatch.setenv("MRF_GRP_FUSE", "0" if grp == "1u" else "1")
     H, W, L, K, per_edge, B = case
     uns, pls, prs = [], [], []
     V = wc0 = None
