@@ -17,7 +17,10 @@
 // edge against 280 for lane = label, 1.57 ms per launch against 2.57; a
 // per-group shared [mu][l] dV accumulator (-DMRF_BGRP_RED=0: 9 KB per warp,
 // 3 CTAs per SM) and data-dependent branches in the gather measured 2-3x
-// slower.
+// slower. FUSE (the direction-0 launches of a call with
+// bwd_grp_fuse()): the sweep also writes the iteration's unary gradient,
+// dtheta(cur) = dtheta_src(cur) + rho sum_{d != 0} A[d](cur) + carry
+// (bwd_small.cuh's fused rule), from a fifth staged row.
 #pragma once
 
 #include <type_traits>
