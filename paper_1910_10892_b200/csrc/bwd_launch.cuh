@@ -111,14 +111,10 @@ static cudaError_t run_grp(const AccArgs& a, int batch, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-inline bool bwd_grp_applies(const AccArgs& a) {
-  return bwd_grp_enabled(a.g.L, a.g.R, a.pot.rho_planes != nullptr);
-}
-
 template <bool TRWP>
 static cudaError_t launch_bwd_sweep(const AccArgs& a, int batch, cudaStream_t s) {
   if (a.nlines == 0) return cudaSuccess;
-  if (TRWP && bwd_uses_small(a.g.L, a.nlines, batch) && bwd_grp_applies(a)) return run_grp(a, batch, s);
+  if (TRWP && bwd_uses_grp(a.g.L, a.g.R, a.pot.rho_planes != nullptr, a.nlines, batch)) return run_grp(a, batch, s);
   // L <= 32 with many lines: one warp per line; few lines: warp-specialised
   if (bwd_uses_small(a.g.L, a.nlines, batch)) {
     if (a.g.R == 4) return run_small<TRWP, 4>(a, batch, s);

@@ -73,6 +73,15 @@ inline bool bwd_grp_enabled(int L, int R, bool rho_planes) {
   if (env && env[0] == '0') return false;
   return R == 4 && L > 16 && L <= 24 && !rho_planes;
 }
+// The grouped kernel takes launches of >= 592 lines (4 per SM) -- C4 on 8
+// GPUs (4 images per rank, 2048 lines): 12.9 ms per backward against 34.6
+// on the warp-specialised kernel; MRF_BWD_SMALL=0 / 1 forces it off / on
+inline bool bwd_uses_grp(int L, int R, bool rho_planes, int nlines, int batch) {
+  if (!bwd_grp_enabled(L, R, rho_planes)) return false;
+  const char* env = getenv("MRF_BWD_SMALL");
+  if (env && (env[0] == '0' || env[0] == '1')) return env[0] == '1';
+  return int64_t(nlines) * batch >= 148 * 4;
+}
 // ... and collects the unary gradient in its direction-0 sweep (A/B:
 // MRF_GRP_FUSE=0 leaves it to dtheta_acc_kernel)
 inline bool bwd_grp_fuse() {

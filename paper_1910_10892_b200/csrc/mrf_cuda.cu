@@ -456,9 +456,9 @@ void run_backward(mrf_topology_t topo, const mrf_problem_f32* pr, int K, const u
       // the warp-specialised kernel's last sweep of the iteration also collects
       // the iteration's unary gradient; the one-warp-per-line kernel leaves it
       // to dtheta_acc_kernel
-      const bool small0 = bwd_uses_small(L, int(topo->dir_lines_all[0].size()), B);
-      const bool fuse = !small0 || bwd_small_fuse() ||
-                        (bwd_grp_enabled(L, R, pr->rho_planes != nullptr) && bwd_grp_fuse());
+      const int lines0 = int(topo->dir_lines_all[0].size());
+      const bool fuse = !bwd_uses_small(L, lines0, B) || bwd_small_fuse() ||
+                        (bwd_uses_grp(L, R, pr->rho_planes != nullptr, lines0, B) && bwd_grp_fuse());
       for (int r = R - 1; r >= 0; --r) {  // directions in reverse (autodiff.hpp:147)
         AccArgs a{g, pot, lines + topo->dir_all_start[r], int(topo->dir_lines_all[r].size()), p, q, k, grad_cost,
                   ain, aout, grads->weight_planes, gvacc, nslots, desc.get(),
